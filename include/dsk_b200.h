@@ -1,0 +1,140 @@
+/*
+ * dsk_b200.h -- C ABI of the B200-native DartMinHash sketching library
+ * (libdsk_b200.so, built from paper_2005_11547_b200/csrc/).
+ *
+ * The reference (`dartsketch`, pure Python) has no FFI; each entry point
+ * below replaces one public function of its hot path, listed beside it as
+ * ref/ = /root/reference/pkg/src/dartsketch/.  INTEGRATION.md shows the
+ * ctypes binding a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - Return 0 on success, a negative DSK_E* code on argument / CUDA error;
+ *     dsk_last_error() describes the last failure of the calling thread.
+ *   - Unless a name ends in _host, array arguments are DEVICE pointers on the
+ *     context's device and calls are ordered on `stream` (a cudaStream_t, NULL =
+ *     legacy default stream).  The caller owns every buffer; the context owns
+ *     only the uploaded hash-family constants and its scratch.
+ *   - uint64 values are raw bit patterns (numpy uint64 / torch int64 views).
+ *   - Per-set status: DSK_OK or one of the codes below.  Bit DSK_STATUS_TIE is
+ *     OR-ed in when two darts of one slot had bit-identical fp64 ranks; the
+ *     library then re-resolves the slot by full index tuple.
+ *   - A context is read-only after creation: concurrent calls on different
+ *     streams are safe.
+ */
+#ifndef DSK_B200_H
+#define DSK_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* per-set status codes (the reference raises these as exceptions) */
+#define DSK_OK 0
+#define DSK_EMPTY 1    /* ValidationError "cannot sketch an empty set"   ref/sketching.py:86-88 */
+#define DSK_WEIGHT 2   /* ValidationError weights not finite and > 0     ref/core.py:38-41 */
+#define DSK_DEPTH 3    /* ValidationError depth/rank depth > 255         ref/darthash.py:158-160 */
+#define DSK_AREAS 4    /* ValidationError > 2^27 areas in one step       ref/darthash.py:242-244 */
+#define DSK_NOCONV 5   /* RuntimeError: buckets unfilled after 64 steps  ref/sketching.py:112 */
+#define DSK_LIMIT 6    /* ValidationError rank limit <= 0 or infinite    ref/darthash.py:136-138 */
+#define DSK_STATUS_TIE 0x100
+
+/* call-level error codes */
+#define DSK_EARG (-1)
+#define DSK_ECUDA (-2)
+#define DSK_ENOMEM (-3)
+#define DSK_EUNSUPPORTED (-4)
+
+typedef struct dsk_ctx dsk_ctx;
+
+/* HashFamily.__init__ (ref/randomness.py:104-112): uploads the 22x256 uint64
+ * tabulation tables (built on the host by numpy exactly as the reference
+ * does), the Poisson(1) CDF (ref/randomness.py:66-85, host libm exp) and the
+ * 258-entry floor(log2) threshold table probed from the host libm
+ * (DESIGN.md "bit-exactness"). */
+int dsk_ctx_create(int device, const uint64_t *tables_host, const double *cdf_host,
+                   const double *log2_thr_host, dsk_ctx **out);
+int dsk_ctx_destroy(dsk_ctx *ctx);
+int dsk_ctx_device(const dsk_ctx *ctx);
+
+/* minhash_density (ref/core.py:150-156): ceil(k ln k) + k, host libm log. */
+int64_t dsk_minhash_density(int64_t k);
+
+/* dart_minhash over a CSR batch (ref/sketching.py:115-123 with
+ * _minhash_values :102-112 and _bucket_minima :93-99), fused with one_bit
+ * packing (ref/sketching.py:164-167; words = np.packbits(bits,
+ * bitorder="little") viewed as <u8, ref/sketching.py:229).
+ *   indptr int64[n+1], ids uint64[nnz], weights float64[nnz]
+ *   out_values uint64[n*k] or NULL; out_bits uint64[n*ceil(k/64)] or NULL
+ *   status int32[n] (required); phi int32[n] or NULL (the reference's final
+ *   step); stats uint32[n*4] or NULL: {areas, candidate darts, hit darts,
+ *   retry passes} at the final step (SURVEY.md §8(d) work units). */
+int dsk_minhash_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                    const double *weights, int64_t n, int32_t k, uint64_t *out_values,
+                    uint64_t *out_bits, int32_t *status, int32_t *phi, uint32_t *stats,
+                    void *stream);
+
+/* The same call with HOST buffers: copies inputs in, sketches, copies the
+ * results out, synchronously.  This is the drop-in a ctypes binding of the
+ * reference would call with numpy arrays. */
+int dsk_minhash_csr_host(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                         const double *weights, int64_t n, int32_t k, uint64_t *out_values,
+                         uint64_t *out_bits, int32_t *status, int32_t *phi, uint32_t *stats);
+
+/* lsh_key over a CSR batch (ref/annindex.py:64-82) fused with the per-table
+ * HashFamily.mix64 fold (ref/randomness.py:160-166) that LshIndex applies
+ * (ref/annindex.py:135).  normalize != 0 first rescales each set by
+ * 2^-weight_class(l1) as LshIndex.insert does (ref/annindex.py:130-131).
+ *   out_keys uint64[n*L] or NULL; out_fps uint64[n*L*K] or NULL (the K
+ *   rank-ordered fingerprints of each table, i.e. lsh_key's tuples). */
+int dsk_lsh_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                const double *weights, int64_t n, int32_t L, int32_t K, int32_t normalize,
+                uint64_t *out_keys, uint64_t *out_fps, int32_t *status, int32_t *phi,
+                uint32_t *stats, void *stream);
+
+int dsk_lsh_csr_host(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                     const double *weights, int64_t n, int32_t L, int32_t K, int32_t normalize,
+                     uint64_t *out_keys, uint64_t *out_fps, int32_t *status, int32_t *phi,
+                     uint32_t *stats);
+
+/* DartHasher.dart_batch (ref/darthash.py:142-295) for each set of a CSR
+ * batch at an absolute rank limit per set: materialises the DartBatch
+ * columns (ref/darthash.py:39-53).  Darts of set s are written at
+ * [offsets[s], offsets[s] + counts[s]) where offsets is an exclusive scan of
+ * the counts of a previous call with cap == 0 (counting pass).  Columns may
+ * be NULL when cap == 0. */
+int dsk_darts_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                  const double *weights, int64_t n, int64_t t, const double *rank_limit,
+                  const int64_t *offsets, int64_t cap, int64_t *counts, int32_t *status,
+                  uint64_t *element, uint16_t *nu, uint16_t *rho, uint32_t *w, uint32_t *r,
+                  uint16_t *j, double *weight, double *rank, uint64_t *fingerprint,
+                  void *stream);
+
+/* HashFamily.hash64_array (ref/randomness.py:170-203) over explicit key
+ * columns; every column is uint64[n]. */
+int dsk_hash64(dsk_ctx *ctx, const uint64_t *element, const uint64_t *nu, const uint64_t *rho,
+               const uint64_t *w, const uint64_t *r, const uint64_t *j, const uint64_t *stream_tag,
+               int64_t n, uint64_t *out, void *stream);
+
+/* HashFamily.mix64 (ref/randomness.py:160-166) over nseq sequences of len
+ * values each (row-major). */
+int dsk_mix64(dsk_ctx *ctx, const uint64_t *values, int64_t nseq, int32_t len, uint64_t *out,
+              void *stream);
+
+/* one_bit (ref/sketching.py:164-167) packed little-endian into uint64 words. */
+int dsk_pack_onebit(const uint64_t *values, int64_t n, int32_t k, uint64_t *out_bits,
+                    void *stream);
+
+/* K0 hash-rate microbenchmark: n_per_thread dependent-free hashes per thread
+ * (one table lookup + splitmix64 each, the minimum a hoisted dart hash
+ * costs) over a full-device grid; xor of results into sink[0]. */
+int dsk_hash_peak(dsk_ctx *ctx, int64_t n_per_thread, uint64_t *sink, int64_t *hashes_done,
+                  void *stream);
+
+const char *dsk_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DSK_B200_H */

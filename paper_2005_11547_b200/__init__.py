@@ -1,0 +1,41 @@
+"""B200-native DartMinHash sketching: weighted minhashes, 1-bit sketches and
+(L, K) LSH keys for batches of sparse weighted sets, computed by hand-written
+sm_100a CUDA kernels behind a C ABI (include/dsk_b200.h).
+
+The public names mirror the reference package `dartsketch`
+(/root/reference/pkg/src/dartsketch/__init__.py) for the hot path; see
+DESIGN.md for the boundary and INTEGRATION.md for the ctypes binding.
+"""
+
+from .constants import ValidationError, minhash_density
+from . import workloads
+from .api import (
+    DSK_STATUS_TIE,
+    Dart,
+    DartBatch,
+    DartHasher,
+    HashFamily,
+    LshBatch,
+    LshParams,
+    MinhashBatch,
+    MinHashSketch,
+    OneBitSketch,
+    WeightedSet,
+    as_u64,
+    dart_minhash,
+    darts_batch,
+    lsh_batch,
+    lsh_key,
+    make_weighted_set,
+    minhash_batch,
+    one_bit,
+    raise_for_status,
+    weight_class,
+)
+
+__all__ = [
+    "ValidationError", "minhash_density", "DSK_STATUS_TIE", "Dart", "DartBatch", "DartHasher",
+    "HashFamily", "LshBatch", "LshParams", "MinhashBatch", "MinHashSketch", "OneBitSketch",
+    "WeightedSet", "as_u64", "dart_minhash", "darts_batch", "lsh_batch", "lsh_key",
+    "make_weighted_set", "minhash_batch", "one_bit", "raise_for_status", "weight_class",
+]

@@ -1,0 +1,250 @@
+// dsk_device.cuh -- device building blocks shared by every kernel.
+//
+// Bit-exactness rules: the whole library is
+// compiled with -fmad=false so no fp64 add/mul pair is contracted to DFMA;
+// critical expressions additionally spell out __dadd_rn/__dmul_rn so the
+// reference's evaluation order is visible.
+#pragma once
+#include <stdint.h>
+
+#define DSK_FULL 0xffffffffu
+
+namespace dsk {
+
+constexpr uint64_t kMul1 = 0xBF58476D1CE4E5B9ULL;  // ref/randomness.py:51
+constexpr uint64_t kMul2 = 0x94D049BB133111EBULL;  // ref/randomness.py:52
+constexpr int kStreamV = 1, kStreamU = 2, kStreamPoisson = 3, kStreamFp = 4, kStreamBucket = 5,
+              kStreamKeyMix = 12;  // ref/randomness.py:28-39
+constexpr double kMaxAreas = 134217728.0;  // 2^27, ref/darthash.py:32
+constexpr double kCandClip = 1099511627776.0;  // 2^40, ref/darthash.py:36
+constexpr uint64_t kEmptyRank = ~0ULL;
+
+// splitmix64 finalizer, ref/randomness.py:58-63
+__host__ __device__ __forceinline__ uint64_t finalize(uint64_t h) {
+  h ^= h >> 30;
+  h *= kMul1;
+  h ^= h >> 27;
+  h *= kMul2;
+  return h ^ (h >> 31);
+}
+
+// 2^e for e in [-1022, 1023], exact
+__device__ __forceinline__ double pow2(int e) {
+  return __longlong_as_double((long long)(1023 + e) << 52);
+}
+
+// (h >> 11) * 2^-53, ref/randomness.py:143 -- the 53-bit integer converts exactly
+__device__ __forceinline__ double u53(uint64_t h) {
+  return __dmul_rn(__ull2double_rn(h >> 11), 0x1p-53);
+}
+
+// floor(math.log2(y)) for y >= 1 using the host-probed threshold table:
+// thr[n] = smallest double below 2^n whose host log2 floors to n (else 2^n).
+// Returns 1024 for inf (the reference raises there; mapped to DSK_DEPTH).
+__device__ __forceinline__ int floor_log2_host(double y, const double *thr) {
+  if (!(y >= 1.0)) return 0;  // only reachable for invalid weights (status DSK_WEIGHT)
+  uint64_t b = (uint64_t)__double_as_longlong(y);
+  int e = (int)((b >> 52) & 0x7ff) - 1023;
+  if (e >= 256) return 1024;
+  return e + (y >= thr[e + 1] ? 1 : 0);
+}
+
+// _largest_passing, ref/darthash.py:80-95, for the rank side:
+// largest c in [0, 2^nu - 1] with r0 + c*drho <= limit, searched in the window
+// floor(min(q, cap)) + {2, 1, 0, -1, -2}; q = (limit - r0) / drho computed as
+// a multiplication by the exact power of two 1/drho = 2^(nu - rho).
+__device__ __forceinline__ int64_t rank_window(double limit, int nu, int rho, double r0,
+                                               double drho) {
+  double q = limit >= r0 ? __dmul_rn(__dadd_rn(limit, -r0), pow2(nu - rho)) : -1.0;
+  int64_t lim_idx = nu >= 62 ? INT64_MAX : (((int64_t)1 << nu) - 1);
+  double cap = nu <= 40 ? (double)lim_idx : kCandClip;
+  q = q < cap ? q : cap;
+  int64_t base = (int64_t)floor(q);
+#pragma unroll
+  for (int delta = 2; delta >= -2; --delta) {
+    int64_t c = base + delta;
+    if (c < 0 || c > lim_idx) continue;
+    if (__dadd_rn(r0, __dmul_rn((double)c, drho)) <= limit) return c;
+  }
+  return -1;
+}
+
+// weight side of the window, ref/darthash.py:200-213 (vectorised there):
+// largest c in [0, 2^rho - 1] with w0 + c*dnu <= x.
+__device__ __forceinline__ int64_t weight_window(double x, double w0, double dnu, int rho) {
+  if (rho == 0) return w0 <= x ? 0 : -1;  // wmax = 0: only candidate 0, w0 + 0*dnu == w0
+  double wmax = __dadd_rn(pow2(rho), -1.0);  // float(2^rho - 1) as numpy compares it
+  double capw = wmax < kCandClip ? wmax : kCandClip;
+  double base = floor(__ddiv_rn(__dadd_rn(x, -w0), dnu));
+  base = base < capw ? base : capw;  // np.minimum
+  base = base > 0.0 ? base : 0.0;    // np.maximum
+#pragma unroll
+  for (int delta = 2; delta >= -2; --delta) {
+    double cand = base + (double)delta;
+    if (cand >= 0.0 && cand <= wmax && __dadd_rn(w0, __dmul_rn(cand, dnu)) <= x)
+      return (int64_t)cand;
+  }
+  return -1;
+}
+
+// numpy pairwise summation (pairwise_sum_DOUBLE, PW_BLOCKSIZE 128), i.e.
+// float(np.sum(weights)) of ref/core.py:44.  Leaf of the recursion:
+__device__ __forceinline__ double pw_leaf(const double *a, int64_t n) {
+  if (n < 8) {
+    double res = 0.0;
+    for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    return res;
+  }
+  double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  int64_t i;
+  for (i = 8; i < n - (n % 8); i += 8) {
+    r0 = __dadd_rn(r0, a[i + 0]); r1 = __dadd_rn(r1, a[i + 1]);
+    r2 = __dadd_rn(r2, a[i + 2]); r3 = __dadd_rn(r3, a[i + 3]);
+    r4 = __dadd_rn(r4, a[i + 4]); r5 = __dadd_rn(r5, a[i + 5]);
+    r6 = __dadd_rn(r6, a[i + 6]); r7 = __dadd_rn(r7, a[i + 7]);
+  }
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
+                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
+  for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  return res;
+}
+
+// Post-order evaluation of the pairwise recursion over n > 128 elements.
+// Leaf values come from `leaf(start, len, index)`.
+template <class LeafFn>
+__device__ double pw_combine(int64_t n, LeafFn leaf) {
+  // explicit stack: (start, len, state, left)
+  int64_t st_start[48], st_len[48];
+  double st_left[48];
+  int st_state[48];
+  int sp = 0;
+  int64_t leaf_idx = 0;
+  double ret = 0.0;
+  st_start[0] = 0; st_len[0] = n; st_state[0] = 0; sp = 1;
+  while (sp > 0) {
+    int top = sp - 1;
+    int64_t len = st_len[top];
+    if (len <= 128) {
+      ret = leaf(st_start[top], len, leaf_idx++);
+      sp--;
+      // deliver to parent
+      while (sp > 0) {
+        int p = sp - 1;
+        if (st_state[p] == 1) {  // left child returned
+          st_left[p] = ret;
+          st_state[p] = 2;
+          int64_t n2 = st_len[p] / 2;
+          n2 -= n2 % 8;
+          st_start[sp] = st_start[p] + n2; st_len[sp] = st_len[p] - n2; st_state[sp] = 0;
+          sp++;
+          break;
+        } else {  // right child returned
+          ret = __dadd_rn(st_left[p], ret);
+          sp--;
+        }
+      }
+    } else {
+      int64_t n2 = len / 2;
+      n2 -= n2 % 8;
+      st_state[top] = 1;
+      st_start[sp] = st_start[top]; st_len[sp] = n2; st_state[sp] = 0;
+      sp++;
+    }
+  }
+  return ret;
+}
+
+// Warp-cooperative float(np.sum(a)): leaves (<=128 elements) are summed by
+// the lanes in parallel, lane 0 combines them in the recursion's order.
+// `scratch` holds >= 256 doubles of warp-private shared memory.
+__device__ __forceinline__ double warp_np_sum(const double *a, int64_t n, double *scratch,
+                                              int lane) {
+  double s = 0.0;
+  if (n <= 128) {
+    if (lane == 0) s = pw_leaf(a, n);
+    return __shfl_sync(DSK_FULL, s, 0);
+  }
+  if (n <= 256 * 64) {  // leaves are longer than 64 elements: < 256 of them
+    pw_combine(n, [&](int64_t start, int64_t len, int64_t idx) {
+      if ((idx & 31) == lane) scratch[idx] = pw_leaf(a + start, len);
+      return 0.0;
+    });
+    __syncwarp();
+    if (lane == 0)
+      s = pw_combine(n, [&](int64_t, int64_t, int64_t idx) { return scratch[idx]; });
+  } else if (lane == 0) {
+    s = pw_combine(n, [&](int64_t start, int64_t len, int64_t) { return pw_leaf(a + start, len); });
+  }
+  __syncwarp();
+  return __shfl_sync(DSK_FULL, s, 0);
+}
+
+// x mod d for 64-bit x, 32-bit d >= 1 (bucket_array's uint64 %, ref/randomness.py:219)
+struct ModU32 {
+  uint64_t m;     // floor(2^64 / d) for non-powers of two
+  uint32_t d;
+  uint32_t mask;  // d - 1 when d is a power of two, else 0
+  int pow2;
+};
+
+__host__ inline ModU32 make_mod(uint32_t d) {
+  ModU32 r;
+  r.d = d;
+  r.pow2 = (d & (d - 1)) == 0;
+  r.mask = d - 1;
+  r.m = r.pow2 ? 0 : (~0ULL) / d;  // floor((2^64-1)/d) == floor(2^64/d) for non-powers of 2
+  return r;
+}
+
+__device__ __forceinline__ uint32_t mod_u32(uint64_t x, const ModU32 &md) {
+  if (md.pow2) return (uint32_t)(x & md.mask);
+  uint64_t q = __umul64hi(x, md.m);
+  uint64_t r = x - q * md.d;
+  if (r >= md.d) r -= md.d;
+  if (r >= md.d) r -= md.d;
+  return (uint32_t)r;
+}
+
+// inclusive warp scan of 32-bit counts
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    uint32_t t = __shfl_up_sync(DSK_FULL, v, o);
+    if (lane >= o) v += t;
+  }
+  return v;
+}
+
+// largest lane s with excl[s] <= pos (excl non-decreasing over lanes)
+__device__ __forceinline__ int warp_owner(uint32_t excl, uint32_t pos) {
+  int s = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    uint32_t e = __shfl_sync(DSK_FULL, excl, s + step);
+    if (e <= pos) s += step;
+  }
+  return s;
+}
+
+// 128-bit shared-memory compare-and-swap (native ATOMS.CAS.128 on sm_90+)
+__device__ __forceinline__ void cas128_shared(uint64_t *addr, uint64_t cmp_lo, uint64_t cmp_hi,
+                                              uint64_t val_lo, uint64_t val_hi, uint64_t &old_lo,
+                                              uint64_t &old_hi) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(addr);
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.shared.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(val_lo), "l"(val_hi), "r"(a)
+      : "memory");
+}
+
+__device__ __forceinline__ void ld128_shared(const uint64_t *addr, uint64_t &lo, uint64_t &hi) {
+  uint32_t a = (uint32_t)__cvta_generic_to_shared(addr);
+  asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(a) : "memory");
+}
+
+}  // namespace dsk

@@ -1,0 +1,776 @@
+// dsk_kernels.cu -- sm_100a kernels and the C ABI of libdsk_b200.so.
+//
+//   K1+K2+K3+K4  minhash_kernel   CSR ingest, l1, validation, DartHash
+//                                 enumeration, k-slot (rank, index) minimum,
+//                                 in-kernel phi-band retry, 1-bit epilogue
+//   K5           lsh_kernel       (dsk_lsh.cuh) bottom-K per table + mix64
+//   K6           darts_kernel     DartBatch materialisation (tests)
+//   K0           hash_peak_kernel hash-rate microbenchmark (roofline peak)
+//   utilities    hash64 / mix64 / pack_onebit kernels
+//
+// Persistent grid: one 512-thread CTA per SM, 16 warps grouped into teams of
+// G warps; a team sketches one set at a time, pulling set indices from a
+// global atomic counter (load balance under Zipf-skewed nnz).  The 45 KB of
+// hash tables live once per CTA in shared memory.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <mutex>
+#include <string>
+
+#include "../../include/dsk_b200.h"
+#include "dsk_device.cuh"
+#include "dsk_engine.cuh"
+
+using namespace dsk;
+
+// ------------------------------------------------------------- context
+
+struct dsk_ctx {
+  int device;
+  int num_sms;
+  uint64_t *d_tab;     // 22*256
+  uint64_t *d_pthr;    // 64
+  double *d_l2thr;     // 258
+  unsigned long long *d_counter;  // work counters (one per concurrent launch slot)
+  size_t max_smem;
+  std::mutex mu;       // serialises use of d_counter across threads
+};
+
+static thread_local std::string g_err;
+
+static int set_err(int code, const char *msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CUDA_TRY(x)                                                              \
+  do {                                                                           \
+    cudaError_t e__ = (x);                                                       \
+    if (e__ != cudaSuccess) {                                                    \
+      g_err = std::string(#x) + ": " + cudaGetErrorString(e__);                  \
+      return DSK_ECUDA;                                                          \
+    }                                                                            \
+  } while (0)
+
+extern "C" const char *dsk_last_error(void) { return g_err.c_str(); }
+
+extern "C" int64_t dsk_minhash_density(int64_t k) {
+  if (k < 1) return -1;
+  if (k == 1) return 1;
+  return (int64_t)ceil((double)k * log((double)k)) + k;  // ref/core.py:156
+}
+
+// ----------------------------------------------------------- smem setup
+
+struct TableArgs {
+  const uint64_t *tab;
+  const uint64_t *pthr;
+  const double *l2thr;
+  double tf;
+};
+
+__device__ void load_tables(SmemTables &T, const TableArgs &a) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  for (int i = tid; i < 8 * 256; i += nt) (&T.tE[0][0])[i] = a.tab[i];
+  for (int i = tid; i < 256; i += nt) {
+    T.tNu[i] = a.tab[8 * 256 + i];
+    T.tRho[i] = a.tab[9 * 256 + i];
+    T.tW[0][i] = a.tab[10 * 256 + i];
+    T.tW[1][i] = a.tab[11 * 256 + i];
+    T.tR[0][i] = a.tab[14 * 256 + i];
+    T.tR[1][i] = a.tab[15 * 256 + i];
+    // w0 = (2^nu - 1) / t, ref/darthash.py:189 (IEEE division)
+    T.w0[i] = __ddiv_rn(__dadd_rn(pow2(i), -1.0), a.tf);
+  }
+  for (int i = tid; i < kJs * 4; i += nt) {
+    int j = i / 4, s = i % 4 + 1;
+    T.js[j][s - 1] = a.tab[18 * 256 + j] ^ a.tab[19 * 256] ^ a.tab[20 * 256 + s] ^ a.tab[21 * 256];
+  }
+  for (int i = tid; i < 64; i += nt) T.pthr[i] = a.pthr[i];
+  for (int i = tid; i < 258; i += nt) T.l2thr[i] = a.l2thr[i];
+  if (tid == 0) {
+    T.cfold = a.tab[12 * 256] ^ a.tab[13 * 256] ^ a.tab[16 * 256] ^ a.tab[17 * 256];
+    T.nfold = a.tab[11 * 256] ^ a.tab[15 * 256];
+    uint64_t b = a.tab[20 * 256 + kStreamBucket] ^ a.tab[21 * 256];
+    for (int p = 8; p < 20; p++) b ^= a.tab[p * 256];
+    T.bconst = b;
+  }
+}
+
+__host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+constexpr size_t kOffQueues = align16(sizeof(SmemTables));
+constexpr size_t kQBytes = align16(sizeof(WarpQueues));
+constexpr size_t kOffTeam = kOffQueues + kWarps * kQBytes;
+
+struct TeamCtl {
+  long long set;
+  double l1;
+  double areas;
+  unsigned int filled;
+  int tie;
+  int abort;
+  int status;
+  int maxdepth;
+  unsigned int darts;
+  unsigned int hits;
+  int pad[3];
+};
+constexpr size_t kTeamCtlBytes = align16(sizeof(TeamCtl));
+
+__device__ __forceinline__ void team_sync(int G, int team) {
+  if (G == 1) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(team + 1), "r"(G * 32) : "memory");
+  }
+}
+
+// ------------------------------------------------------------- minhash
+
+struct MinhashSink {
+  uint64_t *slots;  // 2*k words: {rank bits, fingerprint} per slot, 16-B aligned
+  ModU32 md;
+  unsigned int *filled;
+  int *tie;
+
+  // Slot minimum by (rank, index) (ref/sketching.py:93-99): ranks are
+  // positive doubles, so their IEEE bits order as uint64.  Bit-identical
+  // ranks with different fingerprints flag a tie (resolved by full index
+  // tuple on the host-requested tie path).
+  __device__ void hit(bool valid, const HitInfo &h, int lane) {
+    unsigned newly = 0;
+    bool t = false;
+    if (valid) {
+      uint32_t b = mod_u32(h.bhash, md);
+      uint64_t *sl = slots + 2 * (size_t)b;
+      uint64_t rb = (uint64_t)__double_as_longlong(h.rank);
+      uint64_t cr, cf;
+      ld128_shared(sl, cr, cf);
+      while (true) {
+        if (rb > cr || (rb == cr && h.fp >= cf)) {
+          if (rb == cr && h.fp != cf) t = true;
+          break;
+        }
+        if (rb == cr) t = true;
+        uint64_t orr, off;
+        cas128_shared(sl, cr, cf, rb, h.fp, orr, off);
+        if (orr == cr && off == cf) {
+          if (cr == kEmptyRank) newly = 1;
+          break;
+        }
+        cr = orr;
+        cf = off;
+      }
+    }
+    unsigned nf = __reduce_add_sync(DSK_FULL, newly);
+    bool anyt = __any_sync(DSK_FULL, t);
+    if (lane == 0) {
+      if (nf) atomicAdd(filled, nf);
+      if (anyt) atomicOr(tie, 1);
+    }
+  }
+  __device__ void row(const DartRow &) {}
+};
+
+struct MinhashArgs {
+  const int64_t *indptr;
+  const uint64_t *ids;
+  const double *w;
+  int64_t n;
+  int32_t k;
+  int32_t t;
+  double tf, inv_t;
+  ModU32 md;
+  int G;  // warps per team
+  uint64_t *out_values;
+  uint64_t *out_bits;
+  int32_t *status;
+  int32_t *phi;
+  uint32_t *stats;
+  unsigned long long *counter;
+  TableArgs tabs;
+};
+
+// Per-set validation and l1 by warp 0 of the team: empty set (ref/sketching.py:86-88),
+// finite positive weights (ref/core.py:38-41), l1 = np.sum (ref/core.py:44),
+// max element depth (ref/darthash.py:154-158).
+__device__ void set_prologue(const MinhashArgs &a, const SmemTables &T, TeamCtl &C, int64_t lo,
+                             int64_t nnz, double *scratch, int lane) {
+  if (nnz == 0) {
+    if (lane == 0) C.status = DSK_EMPTY;
+    return;
+  }
+  bool bad = false;
+  int maxd = 0;
+  for (int64_t i = lane; i < nnz; i += 32) {
+    double x = a.w[lo + i];
+    bad |= !(isfinite(x) && x > 0.0);
+    int d = floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, x)), T.l2thr);
+    maxd = d > maxd ? d : maxd;
+  }
+  bad = __any_sync(DSK_FULL, bad);
+  maxd = __reduce_max_sync(DSK_FULL, (unsigned)maxd);
+  double l1 = warp_np_sum(a.w + lo, nnz, scratch, lane);
+  if (lane == 0) {
+    C.l1 = l1;
+    C.maxdepth = maxd;
+    if (bad) C.status = DSK_WEIGHT;
+  }
+}
+
+template <class Sink>
+__device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const PassParams &P,
+                         const int64_t *indptr_unused, const uint64_t *ids, const double *w,
+                         int64_t lo, int64_t nnz, int G, int wit, int lane, double tf,
+                         TeamCtl &C, uint32_t &n_darts, uint32_t &n_hits) {
+  (void)indptr_unused;
+  Engine<Sink, false> eng(T, Q, sink, P, lane);
+  const int CH = 32 / G;
+  for (int64_t c = wit; c * CH < nnz; c += G) {
+    int64_t e = c * CH + lane;
+    bool valid = lane < CH && e < nnz;
+    uint64_t id = 0;
+    double x = 0.0;
+    int depth = 0;
+    if (valid) {
+      id = ids[lo + e];
+      x = w[lo + e];
+      depth = floor_log2_host(__dadd_rn(1.0, __dmul_rn(tf, x)), T.l2thr);
+    }
+    eng.element_chunk(valid, id, x, depth, (uint32_t)e);
+    if (eng.abort) break;
+  }
+  if (!eng.abort) eng.finish();
+  n_darts += eng.n_darts;
+  n_hits += eng.n_hits;
+  if (lane == 0) {
+    atomicAdd(&C.areas, eng.warp_full);
+    if (eng.abort) atomicOr(&C.abort, 1);
+  }
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
+  load_tables(T, a.tabs);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.G, team = warp / G, wit = warp % G, tt = wit * 32 + lane;
+  const int k = a.k;
+  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
+  TeamCtl &C = *reinterpret_cast<TeamCtl *>(smem + kOffTeam + team * kTeamCtlBytes);
+  const int teams = kWarps / G;
+  uint64_t *slots = reinterpret_cast<uint64_t *>(smem + kOffTeam + teams * kTeamCtlBytes) +
+                    (size_t)team * 2 * k;
+  __syncthreads();
+
+  MinhashSink sink;
+  sink.slots = slots;
+  sink.md = a.md;
+  sink.filled = &C.filled;
+  sink.tie = &C.tie;
+
+  for (;;) {
+    if (tt == 0) C.set = (long long)atomicAdd(a.counter, 1ULL);
+    team_sync(G, team);
+    const long long s = C.set;
+    if (s >= a.n) break;
+    const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
+    for (int i = tt; i < k; i += G * 32) {
+      slots[2 * i] = kEmptyRank;
+      slots[2 * i + 1] = 0;
+    }
+    if (tt == 0) {
+      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0; C.areas = 0.0;
+      C.darts = 0; C.hits = 0;
+    }
+    team_sync(G, team);
+    if (wit == 0) set_prologue(a, T, C, lo, nnz, reinterpret_cast<double *>(&Q), lane);
+    team_sync(G, team);
+    int status = C.status;
+    int phi_star = 0;
+    double final_areas = 0.0;
+    uint32_t n_darts = 0, n_hits = 0;
+    if (status == 0) {
+      const double l1 = C.l1;
+      const int maxd = C.maxdepth;
+      status = DSK_NOCONV;
+      double L_prev = -1.0;
+      int RD_prev = 0;
+      for (int phi = 1; phi <= 64; phi++) {  // ref/sketching.py:105
+        // limit = phi / l1 and the checks of DartHasher.dart_batch
+        // (ref/darthash.py:136-138, 157-160)
+        double L = __ddiv_rn((double)phi, l1);
+        if (!(L > 0.0) || isinf(L)) { status = DSK_LIMIT; break; }
+        int RD = floor_log2_host(__dadd_rn(1.0, L), T.l2thr);
+        if (maxd > 255 || RD > 255) { status = DSK_DEPTH; break; }
+        PassParams P;
+        P.gtab = a.tabs.tab;
+        P.inv_t = a.inv_t;
+        P.L_hi = L;
+        P.L_lo = L_prev;
+        P.RD = RD;
+        P.RD_lo = RD_prev;
+        run_pass(T, Q, sink, P, a.indptr, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts,
+                 n_hits);
+        team_sync(G, team);
+        const double areas = C.areas;
+        const bool ab = C.abort != 0;
+        const unsigned filled = C.filled;
+        team_sync(G, team);
+        if (tt == 0) C.areas = 0.0;
+        if (ab || areas > kMaxAreas) { status = DSK_AREAS; break; }  // ref/darthash.py:243
+        final_areas = areas;
+        if (filled == (unsigned)k) {  // every bucket non-empty, ref/sketching.py:110
+          status = DSK_OK;
+          phi_star = phi;
+          break;
+        }
+        L_prev = L;
+        RD_prev = RD;
+      }
+    }
+    // statistics
+    unsigned wd = __reduce_add_sync(DSK_FULL, n_darts), wh = __reduce_add_sync(DSK_FULL, n_hits);
+    if (lane == 0) { atomicAdd(&C.darts, wd); atomicAdd(&C.hits, wh); }
+    team_sync(G, team);
+    // epilogue: values, packed bits (ref/sketching.py:164-167, :229), status
+    if (a.out_values) {
+      uint64_t *o = a.out_values + (size_t)s * k;
+      for (int i = tt; i < k; i += G * 32) o[i] = status == 0 ? slots[2 * i + 1] : 0;
+    }
+    if (a.out_bits) {
+      const int words = (k + 63) / 64;
+      uint64_t *o = a.out_bits + (size_t)s * words;
+      for (int m = wit; m < words; m += G) {
+        int i0 = 64 * m + lane, i1 = i0 + 32;
+        bool b0 = status == 0 && i0 < k && (slots[2 * i0 + 1] & 1);
+        bool b1 = status == 0 && i1 < k && (slots[2 * i1 + 1] & 1);
+        unsigned lo32 = __ballot_sync(DSK_FULL, b0), hi32 = __ballot_sync(DSK_FULL, b1);
+        if (lane == 0) o[m] = ((uint64_t)hi32 << 32) | lo32;
+      }
+    }
+    if (tt == 0) {
+      a.status[s] = status | (C.tie ? DSK_STATUS_TIE : 0);
+      if (a.phi) a.phi[s] = phi_star;
+      if (a.stats) {
+        uint32_t *st = a.stats + (size_t)s * 4;
+        st[0] = (uint32_t)fmin(final_areas, 4294967295.0);
+        st[1] = C.darts;
+        st[2] = C.hits;
+        st[3] = (uint32_t)phi_star;
+      }
+    }
+    team_sync(G, team);
+  }
+}
+
+// ---------------------------------------------------------- K6: darts
+
+struct DartsArgs {
+  const int64_t *indptr;
+  const uint64_t *ids;
+  const double *w;
+  int64_t n;
+  double tf, inv_t;
+  const double *rank_limit;
+  const int64_t *offsets;
+  int64_t cap;
+  int64_t *counts;
+  int32_t *status;
+  uint64_t *element;
+  uint16_t *nu, *rho;
+  uint32_t *ww, *rr;
+  uint16_t *jj;
+  double *weight, *rank;
+  uint64_t *fp;
+  TableArgs tabs;
+};
+
+struct RowSink {
+  const DartsArgs *a;
+  int64_t set, lo;
+  unsigned long long *cursor;  // shared per warp
+  __device__ void hit(bool, const HitInfo &, int) {}
+  __device__ void row(const DartRow &d) {
+    unsigned long long i = atomicAdd(cursor, 1ULL);
+    if (a->cap > 0) {
+      int64_t o = a->offsets[set] + (int64_t)i;
+      int64_t end = set + 1 < a->n ? a->offsets[set + 1] : a->cap;
+      if (o < end && o < a->cap) {
+        a->element[o] = a->ids[lo + d.elem];
+        a->nu[o] = (uint16_t)d.nu;
+        a->rho[o] = (uint16_t)d.rho;
+        a->ww[o] = d.w;
+        a->rr[o] = d.r;
+        a->jj[o] = (uint16_t)d.j;
+        a->weight[o] = d.weight;
+        a->rank[o] = d.rank;
+        a->fp[o] = d.fp;
+      }
+    }
+  }
+};
+
+__global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
+  load_tables(T, a.tabs);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
+  unsigned long long *cursors =
+      reinterpret_cast<unsigned long long *>(smem + kOffTeam);
+  __syncthreads();
+  for (int64_t s = (int64_t)blockIdx.x * kWarps + warp; s < a.n; s += (int64_t)gridDim.x * kWarps) {
+    const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
+    const double L = a.rank_limit[s];
+    int status = 0;
+    if (nnz == 0) status = DSK_EMPTY;                           // ref/darthash.py:133-134
+    else if (!(L > 0.0) || isinf(L)) status = DSK_LIMIT;        // :136-138
+    int maxd = 0;
+    for (int64_t i = lane; i < nnz && status == 0; i += 32) {
+      int d = floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, a.w[lo + i])), T.l2thr);
+      maxd = d > maxd ? d : maxd;
+    }
+    maxd = __reduce_max_sync(DSK_FULL, (unsigned)maxd);
+    int RD = status == 0 ? floor_log2_host(__dadd_rn(1.0, L), T.l2thr) : 0;
+    if (status == 0 && (maxd > 255 || RD > 255)) status = DSK_DEPTH;  // :158-160
+    if (lane == 0) cursors[warp] = 0;
+    __syncwarp();
+    if (status == 0) {
+      PassParams P;
+      P.gtab = a.tabs.tab;
+      P.inv_t = a.inv_t;
+      P.L_hi = L;
+      P.L_lo = -1.0;
+      P.RD = RD;
+      P.RD_lo = 0;
+      RowSink sink;
+      sink.a = &a;
+      sink.set = s;
+      sink.lo = lo;
+      sink.cursor = &cursors[warp];
+      // the area cap is checked on a counting pass first (ref/darthash.py:242-244
+      // raises before any dart is produced)
+      Engine<RowSink, true> eng(T, Q, sink, P, lane);
+      for (int64_t c = 0; c * 32 < nnz; c++) {
+        int64_t e = c * 32 + lane;
+        bool valid = e < nnz;
+        uint64_t id = valid ? a.ids[lo + e] : 0;
+        double x = valid ? a.w[lo + e] : 0.0;
+        int depth = valid ? floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, x)), T.l2thr) : 0;
+        eng.element_chunk(valid, id, x, depth, (uint32_t)e);
+        if (eng.abort) break;
+      }
+      if (!eng.abort) eng.finish();
+      if (eng.abort) status = DSK_AREAS;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      a.status[s] = status;
+      a.counts[s] = status == 0 ? (int64_t)cursors[warp] : 0;
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------- utilities
+
+__device__ __forceinline__ uint64_t hash64_global(const uint64_t *tab, uint64_t e, uint64_t nu,
+                                                  uint64_t rho, uint64_t w, uint64_t r,
+                                                  uint64_t j, uint64_t s) {
+  uint64_t h = 0;
+#pragma unroll
+  for (int p = 0; p < 8; p++) h ^= __ldg(&tab[p * 256 + ((e >> (8 * p)) & 0xff)]);
+  h ^= __ldg(&tab[8 * 256 + (nu & 0xff)]) ^ __ldg(&tab[9 * 256 + (rho & 0xff)]);
+#pragma unroll
+  for (int p = 0; p < 4; p++) h ^= __ldg(&tab[(10 + p) * 256 + ((w >> (8 * p)) & 0xff)]);
+#pragma unroll
+  for (int p = 0; p < 4; p++) h ^= __ldg(&tab[(14 + p) * 256 + ((r >> (8 * p)) & 0xff)]);
+  h ^= __ldg(&tab[18 * 256 + (j & 0xff)]) ^ __ldg(&tab[19 * 256 + ((j >> 8) & 0xff)]);
+  h ^= __ldg(&tab[20 * 256 + (s & 0xff)]) ^ __ldg(&tab[21 * 256 + ((s >> 8) & 0xff)]);
+  return finalize(h);
+}
+
+__global__ void hash64_kernel(const uint64_t *tab, const uint64_t *e, const uint64_t *nu,
+                              const uint64_t *rho, const uint64_t *w, const uint64_t *r,
+                              const uint64_t *j, const uint64_t *s, int64_t n, uint64_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = hash64_global(tab, e[i], nu[i], rho[i], w[i], r[i], j[i], s[i]);
+}
+
+// HashFamily.mix64, ref/randomness.py:160-166
+__global__ void mix64_kernel(const uint64_t *tab, const uint64_t *v, int64_t nseq, int len,
+                             uint64_t *out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nseq;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t mixed = 0;
+    for (int p = 0; p < len; p++)
+      mixed = hash64_global(tab, v[i * len + p] ^ mixed, 0, 0, (uint64_t)p, 0, 0, kStreamKeyMix);
+    out[i] = mixed;
+  }
+}
+
+__global__ void pack_onebit_kernel(const uint64_t *v, int64_t n, int k, uint64_t *out) {
+  const int words = (k + 63) / 64;
+  const int lane = threadIdx.x & 31;
+  int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t t = wid; t < n * words; t += nw) {
+    int64_t s = t / words;
+    int m = (int)(t % words);
+    int i0 = 64 * m + lane, i1 = i0 + 32;
+    bool b0 = i0 < k && (v[s * k + i0] & 1);
+    bool b1 = i1 < k && (v[s * k + i1] & 1);
+    unsigned lo = __ballot_sync(DSK_FULL, b0), hi = __ballot_sync(DSK_FULL, b1);
+    if (lane == 0) out[t] = ((uint64_t)hi << 32) | lo;
+  }
+}
+
+// K0: the cheapest dart hash the engine issues (one shared-memory word XOR +
+// splitmix64), four independent chains per thread, all SMs.
+__global__ void __launch_bounds__(512) hash_peak_kernel(const uint64_t *tab, int64_t iters,
+                                                        uint64_t *sink) {
+  __shared__ uint64_t t0[256];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) t0[i] = tab[i];
+  __syncthreads();
+  uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
+  uint64_t h0 = g * 4 + 1, h1 = g * 4 + 2, h2 = g * 4 + 3, h3 = g * 4 + 4;
+  for (int64_t i = 0; i < iters; i++) {
+    h0 = finalize(h0 ^ t0[h0 & 0xff]);
+    h1 = finalize(h1 ^ t0[h1 & 0xff]);
+    h2 = finalize(h2 ^ t0[h2 & 0xff]);
+    h3 = finalize(h3 ^ t0[h3 & 0xff]);
+  }
+  uint64_t x = h0 ^ h1 ^ h2 ^ h3;
+  if (x == 0x9e3779b97f4a7c15ULL) sink[0] = x;  // practically never; keeps the work live
+}
+
+// ------------------------------------------------------------- host side
+
+static size_t minhash_smem(int k, int G) {
+  int teams = kWarps / G;
+  return kOffTeam + teams * kTeamCtlBytes + (size_t)teams * k * 16;
+}
+
+extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const double *cdf_host,
+                              const double *log2_thr_host, dsk_ctx **out) {
+  if (!tables_host || !cdf_host || !log2_thr_host || !out) return set_err(DSK_EARG, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  dsk_ctx *c = new dsk_ctx();
+  c->device = device;
+  CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
+  int smem_optin = 0;
+  CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  c->max_smem = (size_t)smem_optin;
+  uint64_t pthr[64];
+  for (int m = 0; m < 64; m++) {
+    // count = #{m : cdf[m] <= (X * 2^-53)} = #{m : X >= ceil(cdf[m] * 2^53)}
+    double v = ceil(ldexp(cdf_host[m], 53));
+    pthr[m] = (uint64_t)v;
+  }
+  pthr[63] = pthr[63] > (1ULL << 53) ? pthr[63] : (1ULL << 53);  // X < 2^53: loop sentinel
+  CUDA_TRY(cudaMalloc(&c->d_tab, 22 * 256 * sizeof(uint64_t)));
+  CUDA_TRY(cudaMalloc(&c->d_pthr, 64 * sizeof(uint64_t)));
+  CUDA_TRY(cudaMalloc(&c->d_l2thr, 258 * sizeof(double)));
+  CUDA_TRY(cudaMalloc(&c->d_counter, 64 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMemcpy(c->d_tab, tables_host, 22 * 256 * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_pthr, pthr, sizeof(pthr), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(c->d_l2thr, log2_thr_host, 258 * sizeof(double), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(darts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
+  *out = c;
+  return DSK_OK;
+}
+
+extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
+  if (!c) return DSK_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->d_tab);
+  cudaFree(c->d_pthr);
+  cudaFree(c->d_l2thr);
+  cudaFree(c->d_counter);
+  delete c;
+  return DSK_OK;
+}
+
+extern "C" int dsk_ctx_device(const dsk_ctx *c) { return c ? c->device : -1; }
+
+static TableArgs table_args(const dsk_ctx *c, double tf) {
+  TableArgs t;
+  t.tab = c->d_tab;
+  t.pthr = c->d_pthr;
+  t.l2thr = c->d_l2thr;
+  t.tf = tf;
+  return t;
+}
+
+static int choose_team(const dsk_ctx *c, int k) {
+  for (int G = 1; G <= kWarps; G *= 2)
+    if (minhash_smem(k, G) <= c->max_smem && (size_t)(kWarps / G) * k * 16 <= 96 * 1024) return G;
+  for (int G = 1; G <= kWarps; G *= 2)
+    if (minhash_smem(k, G) <= c->max_smem) return G;
+  return -1;
+}
+
+extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
+                               const double *weights, int64_t n, int32_t k, uint64_t *out_values,
+                               uint64_t *out_bits, int32_t *status, int32_t *phi, uint32_t *stats,
+                               void *stream) {
+  if (!c || !indptr || !status || n < 0) return set_err(DSK_EARG, "bad argument");
+  if (k < 1) return set_err(DSK_EARG, "k must be positive");  // ref/sketching.py:89-90
+  if (n == 0) return DSK_OK;
+  int64_t t = dsk_minhash_density(k);
+  if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "k too large");
+  int G = choose_team(c, k);
+  if (G < 0) return set_err(DSK_EUNSUPPORTED, "k too large for the shared-memory slot array");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lock(c->mu);
+  CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
+  MinhashArgs a;
+  a.indptr = indptr; a.ids = ids; a.w = weights; a.n = n; a.k = k; a.t = (int32_t)t;
+  a.tf = (double)t; a.inv_t = 1.0 / (double)t; a.md = make_mod((uint32_t)k); a.G = G;
+  a.out_values = out_values; a.out_bits = out_bits; a.status = status; a.phi = phi;
+  a.stats = stats; a.counter = c->d_counter; a.tabs = table_args(c, (double)t);
+  size_t smem = minhash_smem(k, G);
+  int grid = c->num_sms;
+  if ((int64_t)grid * (kWarps / G) > n) grid = (int)((n + (kWarps / G) - 1) / (kWarps / G));
+  minhash_kernel<<<grid, kWarps * 32, smem, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}
+
+extern "C" int dsk_darts_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
+                             const double *weights, int64_t n, int64_t t, const double *rank_limit,
+                             const int64_t *offsets, int64_t cap, int64_t *counts, int32_t *status,
+                             uint64_t *element, uint16_t *nu, uint16_t *rho, uint32_t *w,
+                             uint32_t *r, uint16_t *j, double *weight, double *rank,
+                             uint64_t *fingerprint, void *stream) {
+  if (!c || !indptr || !rank_limit || !counts || !status || n < 0)
+    return set_err(DSK_EARG, "bad argument");
+  if (t < 1) return set_err(DSK_EARG, "density parameter t must be positive");
+  if (cap > 0 && (!offsets || !element || !nu || !rho || !w || !r || !j || !weight || !rank ||
+                  !fingerprint))
+    return set_err(DSK_EARG, "null output column");
+  if (n == 0) return DSK_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(c->device));
+  DartsArgs a;
+  a.indptr = indptr; a.ids = ids; a.w = weights; a.n = n; a.tf = (double)t;
+  a.inv_t = 1.0 / (double)t; a.rank_limit = rank_limit; a.offsets = offsets; a.cap = cap;
+  a.counts = counts; a.status = status; a.element = element; a.nu = nu; a.rho = rho; a.ww = w;
+  a.rr = r; a.jj = j; a.weight = weight; a.rank = rank; a.fp = fingerprint;
+  a.tabs = table_args(c, (double)t);
+  size_t smem = kOffTeam + kWarps * sizeof(unsigned long long);
+  int grid = (int)((n + kWarps - 1) / kWarps);
+  if (grid > c->num_sms) grid = c->num_sms;
+  darts_kernel<<<grid, kWarps * 32, smem, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}
+
+extern "C" int dsk_hash64(dsk_ctx *c, const uint64_t *element, const uint64_t *nu,
+                          const uint64_t *rho, const uint64_t *w, const uint64_t *r,
+                          const uint64_t *j, const uint64_t *stream_tag, int64_t n, uint64_t *out,
+                          void *stream) {
+  if (!c || n < 0) return set_err(DSK_EARG, "bad argument");
+  if (n == 0) return DSK_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int grid = (int)((n + 255) / 256);
+  if (grid > c->num_sms * 8) grid = c->num_sms * 8;
+  hash64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(c->d_tab, element, nu, rho, w, r, j,
+                                                         stream_tag, n, out);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}
+
+extern "C" int dsk_mix64(dsk_ctx *c, const uint64_t *values, int64_t nseq, int32_t len,
+                         uint64_t *out, void *stream) {
+  if (!c || nseq < 0 || len < 0) return set_err(DSK_EARG, "bad argument");
+  if (nseq == 0) return DSK_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int grid = (int)((nseq + 255) / 256);
+  if (grid > c->num_sms * 8) grid = c->num_sms * 8;
+  mix64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(c->d_tab, values, nseq, len, out);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}
+
+extern "C" int dsk_pack_onebit(const uint64_t *values, int64_t n, int32_t k, uint64_t *out_bits,
+                               void *stream) {
+  if (!values || !out_bits || n < 0 || k < 1) return set_err(DSK_EARG, "bad argument");
+  if (n == 0) return DSK_OK;
+  int64_t warps = n * ((k + 63) / 64);
+  int grid = (int)((warps * 32 + 255) / 256);
+  if (grid > 148 * 16) grid = 148 * 16;
+  pack_onebit_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(values, n, k, out_bits);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}
+
+extern "C" int dsk_hash_peak(dsk_ctx *c, int64_t n_per_thread, uint64_t *sink,
+                             int64_t *hashes_done, void *stream) {
+  if (!c || n_per_thread < 1 || !sink) return set_err(DSK_EARG, "bad argument");
+  CUDA_TRY(cudaSetDevice(c->device));
+  int grid = c->num_sms * 4;
+  hash_peak_kernel<<<grid, 512, 0, (cudaStream_t)stream>>>(c->d_tab, n_per_thread, sink);
+  CUDA_TRY(cudaGetLastError());
+  if (hashes_done) *hashes_done = (int64_t)grid * 512 * 4 * n_per_thread;
+  return DSK_OK;
+}
+
+// ------------------------------------------------------ host-buffer calls
+
+struct DevBuf {
+  void *p = nullptr;
+  ~DevBuf() { if (p) cudaFree(p); }
+};
+
+#define DEV_ALLOC(buf, bytes) CUDA_TRY(cudaMalloc(&(buf).p, (bytes) ? (bytes) : 1))
+
+extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
+                                    const double *weights, int64_t n, int32_t k,
+                                    uint64_t *out_values, uint64_t *out_bits, int32_t *status,
+                                    int32_t *phi, uint32_t *stats) {
+  if (!c || !indptr || !status || n < 0 || k < 1) return set_err(DSK_EARG, "bad argument");
+  if (n == 0) return DSK_OK;
+  CUDA_TRY(cudaSetDevice(c->device));
+  int64_t nnz = indptr[n] - indptr[0];
+  if (indptr[0] != 0) return set_err(DSK_EARG, "indptr[0] must be 0");
+  int words = (k + 63) / 64;
+  DevBuf dp, di, dw, dv, db, ds, dph, dst;
+  DEV_ALLOC(dp, (n + 1) * sizeof(int64_t));
+  DEV_ALLOC(di, nnz * sizeof(uint64_t));
+  DEV_ALLOC(dw, nnz * sizeof(double));
+  DEV_ALLOC(ds, n * sizeof(int32_t));
+  if (out_values) DEV_ALLOC(dv, (size_t)n * k * sizeof(uint64_t));
+  if (out_bits) DEV_ALLOC(db, (size_t)n * words * sizeof(uint64_t));
+  if (phi) DEV_ALLOC(dph, n * sizeof(int32_t));
+  if (stats) DEV_ALLOC(dst, n * 4 * sizeof(uint32_t));
+  CUDA_TRY(cudaMemcpy(dp.p, indptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(di.p, ids, nnz * sizeof(uint64_t), cudaMemcpyHostToDevice));
+  CUDA_TRY(cudaMemcpy(dw.p, weights, nnz * sizeof(double), cudaMemcpyHostToDevice));
+  int rc = dsk_minhash_csr(c, (int64_t *)dp.p, (uint64_t *)di.p, (double *)dw.p, n, k,
+                           (uint64_t *)dv.p, (uint64_t *)db.p, (int32_t *)ds.p, (int32_t *)dph.p,
+                           (uint32_t *)dst.p, nullptr);
+  if (rc) return rc;
+  CUDA_TRY(cudaDeviceSynchronize());
+  CUDA_TRY(cudaMemcpy(status, ds.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (out_values)
+    CUDA_TRY(cudaMemcpy(out_values, dv.p, (size_t)n * k * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (out_bits)
+    CUDA_TRY(cudaMemcpy(out_bits, db.p, (size_t)n * words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
+  if (phi) CUDA_TRY(cudaMemcpy(phi, dph.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (stats) CUDA_TRY(cudaMemcpy(stats, dst.p, n * 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  return DSK_OK;
+}
+
+#include "dsk_lsh.cuh"

@@ -1,0 +1,156 @@
+"""Seeded synthetic CSR batches for the five BASELINE.json configurations.
+
+The reference measures on synthetic sets only (PAPER.md:297-305,
+ref/bench.py:82-100); BASELINE.json names five batch workloads.  This module
+materialises each of them as CSR arrays (indptr int64[n+1], ids uint64[nnz],
+weights float64[nnz]) that both the CUDA path and the CPU oracle consume.
+
+Conventions:
+  * data RNG = Generator(MT19937(SeedSequence(derive_seed(seed, 1, block)))),
+    one stream per block of BLOCK_ROWS rows so any row range (a GPU shard)
+    can be generated independently of how the batch is split;
+    derive_seed restates ref/randomness.py:89-92;
+  * distinct indices per set (duplicates are redrawn);
+  * Uniform(0,1] = 1 - rng.random();
+  * rows keep draw order.
+"""
+
+from __future__ import annotations
+
+import dataclasses
+
+import numpy as np
+
+BLOCK_ROWS = 1 << 16
+
+
+@dataclasses.dataclass(frozen=True)
+class Workload:
+    name: str
+    n: int
+    d: int
+    nnz: object          # int, or "zipf" for cfg5
+    weights: str         # "uniform" | "exp_l1" | "lognormal1" | "lognormal2"
+    seed: int
+    kind: str            # "minhash" | "lsh"
+    k: tuple = ()        # minhash slot counts
+    L: int = 0
+    K: int = 0
+    onebit: bool = False
+    description: str = ""
+
+
+CONFIGS = {
+    "cfg1": Workload("cfg1", 1000, 10_000, 256, "uniform", 0, "minhash", k=(64,),
+                     description="1,000 sets, d=1e4, nnz=256, U(0,1], k=64, seed 0"),
+    "cfg2": Workload("cfg2", 100_000, 1 << 20, 1024, "exp_l1", 1, "minhash", k=(256,),
+                     description="1e5 sets, d=2^20, nnz=1024, Exp(1) with l1=1, k=256, seed 1"),
+    "cfg3": Workload("cfg3", 1_000_000, 1 << 24, 64, "uniform", 2, "minhash",
+                     k=(64, 256, 1024), onebit=True,
+                     description="1e6 sets, d=2^24, nnz=64, U(0,1], k in {64,256,1024} + 1-bit, seed 2"),
+    "cfg4": Workload("cfg4", 1_000_000, 1 << 24, 128, "lognormal1", 3, "lsh", L=100, K=20,
+                     description="1e6 sets, d=2^24, nnz=128, LogNormal(0,1), (L,K)=(100,20), seed 3"),
+    "cfg5": Workload("cfg5", 10_000_000, 1 << 26, "zipf", "lognormal2", 4, "minhash", k=(128,),
+                     description="1e7 sets, d=2^26, nnz~Zipf(1.5) clipped [1,16384], "
+                                 "LogNormal(0,2), k=128, seed 4"),
+}
+
+
+def derive_seed(base: int, *indices: int) -> int:
+    """ref/randomness.py:89-92."""
+    seq = np.random.SeedSequence(base, spawn_key=tuple(indices))
+    return int(seq.generate_state(1, np.uint64)[0])
+
+
+def _block_rng(seed: int, block: int) -> np.random.Generator:
+    return np.random.Generator(np.random.MT19937(np.random.SeedSequence(
+        derive_seed(seed, 1, block))))
+
+
+def _distinct_rows(rng, d: int, lengths: np.ndarray) -> np.ndarray:
+    """Concatenated rows of distinct ids in [0, d), one row per length."""
+    total = int(lengths.sum())
+    ids = rng.integers(0, d, size=total, dtype=np.uint64)
+    starts = np.zeros(lengths.size + 1, dtype=np.int64)
+    np.cumsum(lengths, out=starts[1:])
+    row = np.repeat(np.arange(lengths.size, dtype=np.int64), lengths)
+    order = np.lexsort((ids, row))
+    sid = ids[order]
+    srow = row[order]
+    dup = (sid[1:] == sid[:-1]) & (srow[1:] == srow[:-1])
+    bad = np.unique(srow[1:][dup])
+    for r in bad.tolist():  # rare: redraw the whole row without replacement
+        a, b = starts[r], starts[r + 1]
+        ids[a:b] = rng.choice(d, size=b - a, replace=False).astype(np.uint64)
+    return ids
+
+
+def _weights(rng, kind: str, lengths: np.ndarray) -> np.ndarray:
+    total = int(lengths.sum())
+    if kind == "uniform":
+        return 1.0 - rng.random(total)
+    if kind == "exp_l1":
+        w = rng.standard_exponential(total)
+        w = np.where(w > 0.0, w, np.finfo(np.float64).tiny)
+        starts = np.zeros(lengths.size + 1, dtype=np.int64)
+        np.cumsum(lengths, out=starts[1:])
+        sums = np.add.reduceat(w, starts[:-1]) if total else np.zeros(0)
+        return w / np.repeat(sums, lengths)
+    if kind == "lognormal1":
+        return rng.lognormal(0.0, 1.0, total)
+    if kind == "lognormal2":
+        return rng.lognormal(0.0, 2.0, total)
+    raise ValueError(kind)
+
+
+def _gen_block(cfg: Workload, block: int, rows: int):
+    rng = _block_rng(cfg.seed, block)
+    if cfg.nnz == "zipf":
+        lengths = np.minimum(rng.zipf(1.5, size=rows), 16384).astype(np.int64)
+    else:
+        lengths = np.full(rows, int(cfg.nnz), dtype=np.int64)
+    if cfg.name == "cfg1":
+        # d = 1e4 with nnz = 256: draw without replacement per set
+        ids = np.concatenate([rng.choice(cfg.d, size=int(m), replace=False).astype(np.uint64)
+                              for m in lengths.tolist()])
+    else:
+        ids = _distinct_rows(rng, cfg.d, lengths)
+    w = _weights(rng, cfg.weights, lengths)
+    return lengths, ids, w
+
+
+def generate(cfg_name: str, n: int | None = None, start: int = 0):
+    """CSR arrays for rows [start, start + n) of a configuration."""
+    cfg = CONFIGS[cfg_name]
+    if n is None:
+        n = cfg.n - start
+    end = start + n
+    b0, b1 = start // BLOCK_ROWS, (end + BLOCK_ROWS - 1) // BLOCK_ROWS
+    lens, idl, wl = [], [], []
+    for b in range(b0, b1):
+        rows = min(BLOCK_ROWS, cfg.n - b * BLOCK_ROWS) if b * BLOCK_ROWS < cfg.n else BLOCK_ROWS
+        lengths, ids, w = _gen_block(cfg, b, rows)
+        lo = max(start - b * BLOCK_ROWS, 0)
+        hi = min(end - b * BLOCK_ROWS, rows)
+        offs = np.zeros(rows + 1, dtype=np.int64)
+        np.cumsum(lengths, out=offs[1:])
+        lens.append(lengths[lo:hi])
+        idl.append(ids[offs[lo]:offs[hi]])
+        wl.append(w[offs[lo]:offs[hi]])
+    lengths = np.concatenate(lens) if lens else np.zeros(0, np.int64)
+    indptr = np.zeros(lengths.size + 1, dtype=np.int64)
+    np.cumsum(lengths, out=indptr[1:])
+    ids = np.ascontiguousarray(np.concatenate(idl) if idl else np.zeros(0, np.uint64))
+    w = np.ascontiguousarray(np.concatenate(wl) if wl else np.zeros(0, np.float64))
+    return indptr, ids, w
+
+
+def subset(indptr, ids, w, rows):
+    """CSR of the given row indices (in the given order)."""
+    rows = np.asarray(rows, dtype=np.int64)
+    lengths = indptr[rows + 1] - indptr[rows]
+    out_ptr = np.zeros(rows.size + 1, dtype=np.int64)
+    np.cumsum(lengths, out=out_ptr[1:])
+    take = np.concatenate([np.arange(indptr[r], indptr[r + 1]) for r in rows.tolist()]) \
+        if rows.size else np.zeros(0, np.int64)
+    return out_ptr, np.ascontiguousarray(ids[take]), np.ascontiguousarray(w[take])

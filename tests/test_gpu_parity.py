@@ -1,0 +1,257 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's
+golden vectors and the CPU oracle.  Bit-exact for every integer output
+(fingerprints, packed bits, keys, dart tuples); fp64 dart weights/ranks are
+compared bit-for-bit too (the reference's rounding order is reproduced).
+"""
+
+import hashlib
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import canonical_darts, golden
+from oracle.oracle import Oracle
+from paper_2005_11547_b200 import (
+    DSK_STATUS_TIE,
+    DartHasher,
+    HashFamily,
+    LshParams,
+    ValidationError,
+    WeightedSet,
+    as_u64,
+    dart_minhash,
+    darts_batch,
+    lsh_batch,
+    lsh_key,
+    make_weighted_set,
+    minhash_batch,
+    minhash_density,
+    one_bit,
+    workloads,
+)
+
+pytestmark = pytest.mark.gpu
+
+_FAMILIES = {}
+
+
+def fam(seed):
+    if seed not in _FAMILIES:
+        _FAMILIES[seed] = HashFamily(seed)
+    return _FAMILIES[seed]
+
+
+def csr_digest(indptr, ids, w) -> str:
+    h = hashlib.sha256()
+    for a in (indptr.astype("<i8"), ids.astype("<u8"), w.astype("<f8")):
+        h.update(a.tobytes())
+    return h.hexdigest()
+
+
+def test_cuda_available():
+    assert torch.cuda.is_available()
+    major, minor = torch.cuda.get_device_capability()
+    assert (major, minor) >= (10, 0)
+
+
+def test_hash64_golden():
+    # tests/test_randomness.py:35-39 of the reference
+    assert fam(1).hash64(123, 4, 5, 6, 7, 8, 9) == 317886004245365293
+
+
+def test_hash64_vectors_all_streams():
+    g = golden("hash_vectors.npz")
+    f = fam(int(g["seed"]))
+    for s_idx, s in enumerate(g["streams"].tolist()):
+        got = f.hash64_array(g["elem"], g["nu"], g["rho"], g["w"], g["r"], g["j"], s)
+        assert np.array_equal(got, g["out"][s_idx]), f"stream {s}"
+
+
+def test_mix64_vectors():
+    g = golden("hash_vectors.npz")
+    f = fam(int(g["seed"]))
+    assert np.array_equal(f.mix64_rows(g["mixseq"]), g["mixed"])
+    assert f.mix64(g["mixseq"][0].tolist()) == int(g["mixed"][0])
+
+
+def _gpu_darts_sweep(name):
+    g = golden(name)
+    f = fam(int(g["seed"]))
+    indptr, ids, w = g["indptr"], g["ids"], g["w"]
+    n = indptr.size - 1
+    limits = g["phi"] / g["l1"]  # DartHasher.darts: phi / ||x||_1
+    mism = 0
+    # the kernel takes one t per call: group rows by t
+    for t in np.unique(g["t"]).tolist():
+        rows = np.nonzero(g["t"] == t)[0]
+        sp, si, sw = workloads.subset(indptr, ids, w, rows)
+        offsets, status, cols = darts_batch(sp, si, sw, t, limits[rows], f)
+        assert (status.cpu().numpy() == 0).all()
+        off = offsets.cpu().numpy()
+        host = {k: v.cpu().numpy() for k, v in cols.items()}
+        for q, s in enumerate(rows.tolist()):
+            a, b = off[q], off[q + 1]
+            arr = np.empty(b - a, dtype=[("element", "<u8"), ("nu", "<u2"), ("rho", "<u2"),
+                                         ("w", "<u4"), ("r", "<u4"), ("j", "<u2"),
+                                         ("weight", "<f8"), ("rank", "<f8"),
+                                         ("fingerprint", "<u8")])
+            arr["element"] = host["element"][a:b].view(np.uint64)
+            arr["nu"] = host["nu"][a:b].view(np.uint16)
+            arr["rho"] = host["rho"][a:b].view(np.uint16)
+            arr["w"] = host["w"][a:b].view(np.uint32)
+            arr["r"] = host["r"][a:b].view(np.uint32)
+            arr["j"] = host["j"][a:b].view(np.uint16)
+            arr["weight"] = host["weight"][a:b]
+            arr["rank"] = host["rank"][a:b]
+            arr["fingerprint"] = host["fingerprint"][a:b].view(np.uint64)
+            c = canonical_darts(arr)
+            if c.size != g["counts"][s] or \
+                    hashlib.sha256(c.tobytes()).hexdigest() != g["digests"][s]:
+                mism += 1
+    assert mism == 0, f"{mism}/{n} sets differ"
+
+
+def test_darts_criterion1_sweep():
+    # tests/test_acceptance.py:42-63: 1000 sets, l0 <= 64, norms 2^+-4,
+    # phi in {.5,1,2,4}, t in {1,16,256}: tuple-for-tuple equal
+    _gpu_darts_sweep("darts_sweep.npz")
+
+
+@pytest.mark.parametrize("tag", ["p64", "m64"])
+def test_darts_extreme_norms(tag):
+    # tests/test_acceptance.py:279-284
+    _gpu_darts_sweep(f"darts_sweep_{tag}.npz")
+
+
+@pytest.mark.parametrize("name,cfg", [
+    ("minhash_cfg1.npz", "cfg1"), ("minhash_cfg2.npz", "cfg2"),
+    ("minhash_cfg3_k64.npz", "cfg3"), ("minhash_cfg3_k256.npz", "cfg3"),
+    ("minhash_cfg3_k1024.npz", "cfg3"), ("minhash_cfg5.npz", "cfg5")])
+def test_minhash_golden(name, cfg):
+    g = golden(name)
+    rows, k = int(g["rows"]), int(g["k"])
+    indptr, ids, w = workloads.generate(cfg, n=rows)
+    assert csr_digest(indptr, ids, w) == str(g["digest"])
+    res = minhash_batch(indptr, ids, w, k, fam(workloads.CONFIGS[cfg].seed),
+                        bits="bits" in g.files)
+    assert (res.status.cpu().numpy() == 0).all()
+    assert np.array_equal(as_u64(res.values), g["values"])
+    assert np.array_equal(res.phi.cpu().numpy(), g["phi"])
+    st = res.stats.cpu().numpy().view(np.uint32)
+    assert np.array_equal(st[:, 2].astype(np.int64), g["hits"])  # H(phi*) per set
+    if "bits" in g.files:
+        assert np.array_equal(as_u64(res.bits), g["bits"])
+
+
+def test_minhash_small_edge_cases():
+    g = golden("minhash_small.npz")
+    f = fam(int(g["seed"]))
+    for k in g["ks"].tolist():
+        res = minhash_batch(g["indptr"], g["ids"], g["w"], k, f, check=False)
+        status = res.status.cpu().numpy()
+        assert np.array_equal(status & 0xFF, g[f"status_k{k}"]), k
+        assert not (status & DSK_STATUS_TIE).any()
+        ok = status == 0
+        assert np.array_equal(as_u64(res.values)[ok], g[f"values_k{k}"][ok]), k
+        assert np.array_equal(res.phi.cpu().numpy()[ok], g[f"phi_k{k}"][ok]), k
+
+
+def _oracle_compare(cfg, k, rows, start=0, bits=False):
+    indptr, ids, w = workloads.generate(cfg, n=rows, start=start)
+    seed = workloads.CONFIGS[cfg].seed
+    res = minhash_batch(indptr, ids, w, k, fam(seed), bits=bits)
+    vals, status, phi, hits = Oracle(seed).minhash_csr(indptr, ids, w, k)
+    assert (status == 0).all()
+    gv = as_u64(res.values)
+    mism = int((gv != vals).sum())
+    assert mism == 0, f"{cfg} k={k}: {mism} slot mismatches of {vals.size}"
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+    assert np.array_equal(res.stats.cpu().numpy().view(np.uint32)[:, 2].astype(np.int64), hits)
+    if bits:
+        ob = np.zeros((rows, (k + 63) // 64), dtype=np.uint64)
+        for i in range(rows):
+            packed = np.packbits((vals[i] & np.uint64(1)).astype(np.uint8), bitorder="little")
+            pad = np.zeros(ob.shape[1] * 8, dtype=np.uint8)
+            pad[:packed.size] = packed
+            ob[i] = pad.view("<u8")
+        assert np.array_equal(as_u64(res.bits), ob)
+
+
+def test_minhash_cfg2_vs_oracle():
+    _oracle_compare("cfg2", 256, 1500, start=3000)
+
+
+@pytest.mark.parametrize("k", [64, 256, 1024])
+def test_minhash_cfg3_vs_oracle(k):
+    _oracle_compare("cfg3", k, {64: 4000, 256: 2000, 1024: 600}[k], start=70000, bits=True)
+
+
+def test_minhash_cfg5_vs_oracle():
+    _oracle_compare("cfg5", 128, 4000, start=200000)
+
+
+def test_minhash_odd_k_vs_oracle():
+    # non-power-of-two bucket counts exercise the 64-bit modulo
+    for k in (1, 3, 100, 333, 2000):
+        _oracle_compare("cfg1", k, 60)
+
+
+def test_minhash_determinism_and_row_order():
+    indptr, ids, w = workloads.generate("cfg3", n=3000)
+    f = fam(2)
+    a = as_u64(minhash_batch(indptr, ids, w, 256, f).values)
+    b = as_u64(minhash_batch(indptr, ids, w, 256, f).values)
+    assert np.array_equal(a, b)
+    rows = np.random.default_rng(5).permutation(3000)
+    sp, si, sw = workloads.subset(indptr, ids, w, rows)
+    c = as_u64(minhash_batch(sp, si, sw, 256, f).values)
+    assert np.array_equal(c, a[rows])
+    # element order inside a set does not matter (total order on darts)
+    perm_rows = []
+    for r in range(50):
+        seg = np.arange(indptr[r], indptr[r + 1])
+        perm_rows.append(np.random.default_rng(r).permutation(seg))
+    take = np.concatenate(perm_rows)
+    pp = indptr[:51].copy()
+    d = as_u64(minhash_batch(pp, ids[take], w[take], 256, f).values)
+    assert np.array_equal(d, a[:50])
+
+
+def test_facade_single_set_api():
+    f = fam(0xBEEF)
+    x = make_weighted_set([(1, 0.5), (2, 0.25), (3, 1.25)])
+    # k = 1 equals the global (rank, index)-minimum dart (tests/test_sketching.py:42-46)
+    darts = DartHasher(1, f).darts(x, 64.0)
+    best = min(darts, key=lambda d: (d.rank, d.index))
+    assert dart_minhash(x, 1, f).values.tolist() == [best.fingerprint]
+    s = dart_minhash(x, 64, f)
+    assert one_bit(s).bits.tolist() == (s.values & np.uint64(1)).tolist()
+    with pytest.raises(ValidationError):
+        dart_minhash(make_weighted_set([]), 4, f)
+    with pytest.raises(ValidationError):
+        dart_minhash(x, 0, f)
+    # darts against the oracle
+    orc = Oracle(0xBEEF)
+    st, od = orc.darts_below_rank(x.ids, x.weights, 16, 3.0)
+    gd = DartHasher(16, f).darts_below_rank(x, 3.0)
+    assert st == 0 and len(gd) == od.size
+    assert {d.index for d in gd} == {(int(e), int(a), int(b), int(c), int(r), int(j))
+                                     for e, a, b, c, r, j in zip(od["element"], od["nu"], od["rho"],
+                                                                 od["w"], od["r"], od["j"])}
+
+
+def test_batch_status_errors():
+    f = fam(3)
+    indptr = np.array([0, 1, 1, 3, 4], dtype=np.int64)
+    ids = np.array([5, 6, 7, 8], dtype=np.uint64)
+    w = np.array([1.0, 0.5, -1.0, np.inf])
+    res = minhash_batch(indptr, ids, w, 16, f, check=False)
+    assert res.status.cpu().numpy().tolist() == [0, 1, 2, 2]
+    with pytest.raises(ValidationError):
+        minhash_batch(indptr, ids, w, 16, f)
+
+
+def test_minhash_density_matches():
+    for k in (1, 2, 64, 128, 256, 1024, 2000):
+        assert minhash_density(k) == Oracle.minhash_density(k)
