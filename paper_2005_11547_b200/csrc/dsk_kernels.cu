@@ -18,6 +18,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <atomic>
 #include <mutex>
 #include <string>
 
@@ -35,10 +36,18 @@ struct dsk_ctx {
   uint64_t *d_tab;     // 22*256
   uint64_t *d_pthr;    // 64
   double *d_l2thr;     // 258
-  unsigned long long *d_counter;  // work counters (one per concurrent launch slot)
+  unsigned long long *d_counter;  // kCounterSlots work counters, one per in-flight launch
+  std::atomic<unsigned> next_slot{0};
   size_t max_smem;
-  std::mutex mu;       // serialises use of d_counter across threads
+  // host-buffer path: device staging owned by the context
+  std::mutex host_mu;
+  void *stage = nullptr;
+  size_t stage_bytes = 0;
+  cudaStream_t hs[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[2] = {nullptr, nullptr};
 };
+
+constexpr int kCounterSlots = 256;
 
 static thread_local std::string g_err;
 
@@ -578,7 +587,7 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
   CUDA_TRY(cudaMalloc(&c->d_tab, 22 * 256 * sizeof(uint64_t)));
   CUDA_TRY(cudaMalloc(&c->d_pthr, 64 * sizeof(uint64_t)));
   CUDA_TRY(cudaMalloc(&c->d_l2thr, 258 * sizeof(double)));
-  CUDA_TRY(cudaMalloc(&c->d_counter, 64 * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&c->d_counter, kCounterSlots * sizeof(unsigned long long)));
   CUDA_TRY(cudaMemcpy(c->d_tab, tables_host, 22 * 256 * sizeof(uint64_t), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c->d_pthr, pthr, sizeof(pthr), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c->d_l2thr, log2_thr_host, 258 * sizeof(double), cudaMemcpyHostToDevice));
@@ -597,6 +606,11 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
   cudaFree(c->d_pthr);
   cudaFree(c->d_l2thr);
   cudaFree(c->d_counter);
+  if (c->stage) cudaFree(c->stage);
+  for (int i = 0; i < 2; i++) {
+    if (c->hs[i]) cudaStreamDestroy(c->hs[i]);
+    if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+  }
   delete c;
   return DSK_OK;
 }
@@ -633,13 +647,15 @@ extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
   if (G < 0) return set_err(DSK_EUNSUPPORTED, "k too large for the shared-memory slot array");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
-  std::lock_guard<std::mutex> lock(c->mu);
-  CUDA_TRY(cudaMemsetAsync(c->d_counter, 0, sizeof(unsigned long long), st));
+  // each launch owns one counter slot; slots recycle after kCounterSlots launches,
+  // far beyond the number that can be in flight
+  unsigned long long *counter = c->d_counter + (c->next_slot.fetch_add(1) % kCounterSlots);
+  CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   MinhashArgs a;
   a.indptr = indptr; a.ids = ids; a.w = weights; a.n = n; a.k = k; a.t = (int32_t)t;
   a.tf = (double)t; a.inv_t = 1.0 / (double)t; a.md = make_mod((uint32_t)k); a.G = G;
   a.out_values = out_values; a.out_bits = out_bits; a.status = status; a.phi = phi;
-  a.stats = stats; a.counter = c->d_counter; a.tabs = table_args(c, (double)t);
+  a.stats = stats; a.counter = counter; a.tabs = table_args(c, (double)t);
   size_t smem = minhash_smem(k, G);
   int grid = c->num_sms;
   if ((int64_t)grid * (kWarps / G) > n) grid = (int)((n + (kWarps / G) - 1) / (kWarps / G));
@@ -728,13 +744,49 @@ extern "C" int dsk_hash_peak(dsk_ctx *c, int64_t n_per_thread, uint64_t *sink,
 }
 
 // ------------------------------------------------------ host-buffer calls
+//
+// dsk_*_csr_host: the drop-in for a caller holding numpy arrays.  Rows are
+// cut into chunks of ~64 MB of input; chunk c is copied in, sketched and
+// copied out on stream c % 2, so the PCIe transfers of one chunk overlap the
+// kernel of the other.  Device staging is owned by the context and reused.
 
-struct DevBuf {
-  void *p = nullptr;
-  ~DevBuf() { if (p) cudaFree(p); }
-};
+static int ensure_stage(dsk_ctx *c, size_t bytes) {
+  if (c->stage_bytes >= bytes) return DSK_OK;
+  if (c->stage) CUDA_TRY(cudaFree(c->stage));
+  c->stage = nullptr;
+  c->stage_bytes = 0;
+  CUDA_TRY(cudaMalloc(&c->stage, bytes));
+  c->stage_bytes = bytes;
+  if (!c->hs[0]) {
+    for (int i = 0; i < 2; i++) {
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->hs[i], cudaStreamNonBlocking));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+    }
+  }
+  return DSK_OK;
+}
 
-#define DEV_ALLOC(buf, bytes) CUDA_TRY(cudaMalloc(&(buf).p, (bytes) ? (bytes) : 1))
+// Row chunk boundaries with ~target input bytes per chunk.
+static void plan_chunks(const int64_t *indptr, int64_t n, size_t target, int64_t *bounds,
+                        int max_chunks, int *nchunks) {
+  int m = 0;
+  bounds[m++] = 0;
+  int64_t r = 0;
+  while (r < n && m < max_chunks) {
+    int64_t lo = r;
+    // advance until ~target bytes (16 B per nonzero + 8 B per row)
+    int64_t step = 1;
+    while (r < n && (size_t)((indptr[r] - indptr[lo]) * 16 + (r - lo) * 8) < target) {
+      int64_t nr = r + step < n ? r + step : n;
+      r = nr;
+      step = step < (1 << 16) ? step * 2 : step;
+    }
+    if (r == lo) r = lo + 1;
+    bounds[m++] = r;
+  }
+  if (bounds[m - 1] != n) bounds[m - 1] = n;
+  *nchunks = m - 1;
+}
 
 extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                                     const double *weights, int64_t n, int32_t k,
@@ -742,34 +794,60 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
                                     int32_t *phi, uint32_t *stats) {
   if (!c || !indptr || !status || n < 0 || k < 1) return set_err(DSK_EARG, "bad argument");
   if (n == 0) return DSK_OK;
-  CUDA_TRY(cudaSetDevice(c->device));
-  int64_t nnz = indptr[n] - indptr[0];
   if (indptr[0] != 0) return set_err(DSK_EARG, "indptr[0] must be 0");
-  int words = (k + 63) / 64;
-  DevBuf dp, di, dw, dv, db, ds, dph, dst;
-  DEV_ALLOC(dp, (n + 1) * sizeof(int64_t));
-  DEV_ALLOC(di, nnz * sizeof(uint64_t));
-  DEV_ALLOC(dw, nnz * sizeof(double));
-  DEV_ALLOC(ds, n * sizeof(int32_t));
-  if (out_values) DEV_ALLOC(dv, (size_t)n * k * sizeof(uint64_t));
-  if (out_bits) DEV_ALLOC(db, (size_t)n * words * sizeof(uint64_t));
-  if (phi) DEV_ALLOC(dph, n * sizeof(int32_t));
-  if (stats) DEV_ALLOC(dst, n * 4 * sizeof(uint32_t));
-  CUDA_TRY(cudaMemcpy(dp.p, indptr, (n + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(di.p, ids, nnz * sizeof(uint64_t), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaMemcpy(dw.p, weights, nnz * sizeof(double), cudaMemcpyHostToDevice));
-  int rc = dsk_minhash_csr(c, (int64_t *)dp.p, (uint64_t *)di.p, (double *)dw.p, n, k,
-                           (uint64_t *)dv.p, (uint64_t *)db.p, (int32_t *)ds.p, (int32_t *)dph.p,
-                           (uint32_t *)dst.p, nullptr);
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lock(c->host_mu);
+  const int64_t nnz = indptr[n];
+  const int words = (k + 63) / 64;
+  // device layout: indptr | ids | w | values | bits | status | phi | stats
+  size_t off_p = 0, off_i = align16((n + 1) * 8), off_w = off_i + align16(nnz * 8);
+  size_t off_v = off_w + align16(nnz * 8);
+  size_t off_b = off_v + (out_values ? align16((size_t)n * k * 8) : 0);
+  size_t off_s = off_b + (out_bits ? align16((size_t)n * words * 8) : 0);
+  size_t off_ph = off_s + align16(n * 4);
+  size_t off_st = off_ph + (phi ? align16(n * 4) : 0);
+  size_t total = off_st + (stats ? align16(n * 16) : 0);
+  int rc = ensure_stage(c, total);
   if (rc) return rc;
-  CUDA_TRY(cudaDeviceSynchronize());
-  CUDA_TRY(cudaMemcpy(status, ds.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (out_values)
-    CUDA_TRY(cudaMemcpy(out_values, dv.p, (size_t)n * k * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-  if (out_bits)
-    CUDA_TRY(cudaMemcpy(out_bits, db.p, (size_t)n * words * sizeof(uint64_t), cudaMemcpyDeviceToHost));
-  if (phi) CUDA_TRY(cudaMemcpy(phi, dph.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
-  if (stats) CUDA_TRY(cudaMemcpy(stats, dst.p, n * 4 * sizeof(uint32_t), cudaMemcpyDeviceToHost));
+  char *base = (char *)c->stage;
+  int64_t *dp = (int64_t *)(base + off_p);
+  uint64_t *di = (uint64_t *)(base + off_i);
+  double *dw = (double *)(base + off_w);
+  uint64_t *dv = out_values ? (uint64_t *)(base + off_v) : nullptr;
+  uint64_t *db = out_bits ? (uint64_t *)(base + off_b) : nullptr;
+  int32_t *ds = (int32_t *)(base + off_s);
+  int32_t *dph = phi ? (int32_t *)(base + off_ph) : nullptr;
+  uint32_t *dst = stats ? (uint32_t *)(base + off_st) : nullptr;
+  constexpr int kMaxChunks = 64;
+  int64_t bounds[kMaxChunks + 1];
+  int nch = 0;
+  plan_chunks(indptr, n, (size_t)64 << 20, bounds, kMaxChunks + 1, &nch);
+  CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, c->hs[0]));
+  CUDA_TRY(cudaEventRecord(c->ev_in[0], c->hs[0]));
+  CUDA_TRY(cudaStreamWaitEvent(c->hs[1], c->ev_in[0], 0));
+  for (int ch = 0; ch < nch; ch++) {
+    cudaStream_t st = c->hs[ch & 1];
+    int64_t r0 = bounds[ch], r1 = bounds[ch + 1], m = r1 - r0;
+    int64_t e0 = indptr[r0], e1 = indptr[r1];
+    CUDA_TRY(cudaMemcpyAsync(di + e0, ids + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(dw + e0, weights + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, st));
+    rc = dsk_minhash_csr(c, dp + r0, di, dw, m, k, dv ? dv + r0 * k : nullptr,
+                         db ? db + r0 * words : nullptr, ds + r0, dph ? dph + r0 : nullptr,
+                         dst ? dst + r0 * 4 : nullptr, st);
+    if (rc) return rc;
+    if (out_values)
+      CUDA_TRY(cudaMemcpyAsync(out_values + r0 * k, dv + r0 * k, (size_t)m * k * 8,
+                               cudaMemcpyDeviceToHost, st));
+    if (out_bits)
+      CUDA_TRY(cudaMemcpyAsync(out_bits + r0 * words, db + r0 * words, (size_t)m * words * 8,
+                               cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(status + r0, ds + r0, m * 4, cudaMemcpyDeviceToHost, st));
+    if (phi) CUDA_TRY(cudaMemcpyAsync(phi + r0, dph + r0, m * 4, cudaMemcpyDeviceToHost, st));
+    if (stats)
+      CUDA_TRY(cudaMemcpyAsync(stats + r0 * 4, dst + r0 * 4, m * 16, cudaMemcpyDeviceToHost, st));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->hs[0]));
+  CUDA_TRY(cudaStreamSynchronize(c->hs[1]));
   return DSK_OK;
 }
 

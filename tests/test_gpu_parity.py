@@ -255,3 +255,28 @@ def test_batch_status_errors():
 def test_minhash_density_matches():
     for k in (1, 2, 64, 128, 256, 1024, 2000):
         assert minhash_density(k) == Oracle.minhash_density(k)
+
+
+def test_host_buffer_abi_matches_device_path():
+    """dsk_minhash_csr_host (numpy buffers, chunked pipeline) == device path."""
+    import ctypes
+
+    from paper_2005_11547_b200 import _lib
+    indptr, ids, w = workloads.generate("cfg2", n=9000)
+    f = fam(1)
+    k = 256
+    dev = minhash_batch(indptr, ids, w, k, f, bits=True)
+    vals = np.zeros((9000, k), dtype=np.uint64)
+    bits = np.zeros((9000, 4), dtype=np.uint64)
+    status = np.zeros(9000, dtype=np.int32)
+    phi = np.zeros(9000, dtype=np.int32)
+    stats = np.zeros((9000, 4), dtype=np.uint32)
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    rc = _lib.load().dsk_minhash_csr_host(f.context(), P(indptr), P(ids), P(w), 9000, k, P(vals),
+                                         P(bits), P(status), P(phi), P(stats))
+    assert rc == 0
+    assert (status == 0).all()
+    assert np.array_equal(vals, as_u64(dev.values))
+    assert np.array_equal(bits, as_u64(dev.bits))
+    assert np.array_equal(phi, dev.phi.cpu().numpy())
+    assert np.array_equal(stats, dev.stats.cpu().numpy().view(np.uint32))
