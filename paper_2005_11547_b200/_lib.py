@@ -18,7 +18,8 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_PATH = os.path.join(PKG, "libdsk_b200.so")
 HEADER = os.path.join(REPO, "include", "dsk_b200.h")
-SOURCES = ["dsk_kernels.cu", "dsk_device.cuh", "dsk_engine.cuh", "dsk_lsh.cuh"]
+SOURCES = ["dsk_kernels.cu", "dsk_device.cuh", "dsk_engine.cuh", "dsk_lsh_kernel.cuh",
+           "dsk_lsh_host.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

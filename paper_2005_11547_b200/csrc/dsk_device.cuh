@@ -70,12 +70,22 @@ __device__ __forceinline__ int64_t rank_window(double limit, int nu, int rho, do
 }
 
 // weight side of the window, ref/darthash.py:200-213 (vectorised there):
-// largest c in [0, 2^rho - 1] with w0 + c*dnu <= x.
-__device__ __forceinline__ int64_t weight_window(double x, double w0, double dnu, int rho) {
+// largest c in [0, 2^rho - 1] with w0 + c*dnu <= x, searched in the window
+// clamp(floor((x - w0) / dnu)) + {2, 1, 0, -1, -2}.
+//
+// The estimate uses a multiplication by tpow = t * 2^(rho - nu) instead of
+// the IEEE division by dnu = fl(1/t) * 2^(nu - rho).  Both quotients are
+// within 3 ulps of the true (x - w0)/dnu, so for every legal step (area
+// count <= 2^27, hence quotients < 2^50) their floors differ by at most one
+// and both windows contain the true largest passing c; the predicate is
+// monotone in c, so the first passing candidate is that same c.  Steps where
+// the quotient is >= 2^50 clamp both estimates identically (wmax or 2^40).
+__device__ __forceinline__ int64_t weight_window(double x, double w0, double dnu, double tpow,
+                                                 int rho) {
   if (rho == 0) return w0 <= x ? 0 : -1;  // wmax = 0: only candidate 0, w0 + 0*dnu == w0
   double wmax = __dadd_rn(pow2(rho), -1.0);  // float(2^rho - 1) as numpy compares it
   double capw = wmax < kCandClip ? wmax : kCandClip;
-  double base = floor(__ddiv_rn(__dadd_rn(x, -w0), dnu));
+  double base = floor(__dmul_rn(__dadd_rn(x, -w0), tpow));
   base = base < capw ? base : capw;  // np.minimum
   base = base > 0.0 ? base : 0.0;    // np.maximum
 #pragma unroll
@@ -89,23 +99,28 @@ __device__ __forceinline__ int64_t weight_window(double x, double w0, double dnu
 
 // numpy pairwise summation (pairwise_sum_DOUBLE, PW_BLOCKSIZE 128), i.e.
 // float(np.sum(weights)) of ref/core.py:44.  Leaf of the recursion:
-__device__ __forceinline__ double pw_leaf(const double *a, int64_t n) {
+// (`sexp` != 0 sums the values rescaled by 2^sexp, i.e. np.sum(np.ldexp(a, sexp)).)
+__device__ __forceinline__ double pw_ld(const double *a, int64_t i, int sexp) {
+  return sexp ? scalbn(a[i], sexp) : a[i];
+}
+
+__device__ __forceinline__ double pw_leaf(const double *a, int64_t n, int sexp) {
   if (n < 8) {
     double res = 0.0;
-    for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, a[i]);
+    for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, pw_ld(a, i, sexp));
     return res;
   }
-  double r0 = a[0], r1 = a[1], r2 = a[2], r3 = a[3], r4 = a[4], r5 = a[5], r6 = a[6], r7 = a[7];
+  double r[8];
+#pragma unroll
+  for (int j = 0; j < 8; j++) r[j] = pw_ld(a, j, sexp);
   int64_t i;
   for (i = 8; i < n - (n % 8); i += 8) {
-    r0 = __dadd_rn(r0, a[i + 0]); r1 = __dadd_rn(r1, a[i + 1]);
-    r2 = __dadd_rn(r2, a[i + 2]); r3 = __dadd_rn(r3, a[i + 3]);
-    r4 = __dadd_rn(r4, a[i + 4]); r5 = __dadd_rn(r5, a[i + 5]);
-    r6 = __dadd_rn(r6, a[i + 6]); r7 = __dadd_rn(r7, a[i + 7]);
+#pragma unroll
+    for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], pw_ld(a, i + j, sexp));
   }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r0, r1), __dadd_rn(r2, r3)),
-                         __dadd_rn(__dadd_rn(r4, r5), __dadd_rn(r6, r7)));
-  for (; i < n; i++) res = __dadd_rn(res, a[i]);
+  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
+                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
+  for (; i < n; i++) res = __dadd_rn(res, pw_ld(a, i, sexp));
   return res;
 }
 
@@ -158,22 +173,24 @@ __device__ double pw_combine(int64_t n, LeafFn leaf) {
 // the lanes in parallel, lane 0 combines them in the recursion's order.
 // `scratch` holds >= 256 doubles of warp-private shared memory.
 __device__ __forceinline__ double warp_np_sum(const double *a, int64_t n, double *scratch,
-                                              int lane) {
+                                              int lane, int sexp) {
   double s = 0.0;
   if (n <= 128) {
-    if (lane == 0) s = pw_leaf(a, n);
+    if (lane == 0) s = pw_leaf(a, n, sexp);
     return __shfl_sync(DSK_FULL, s, 0);
   }
   if (n <= 256 * 64) {  // leaves are longer than 64 elements: < 256 of them
     pw_combine(n, [&](int64_t start, int64_t len, int64_t idx) {
-      if ((idx & 31) == lane) scratch[idx] = pw_leaf(a + start, len);
+      if ((idx & 31) == lane) scratch[idx] = pw_leaf(a + start, len, sexp);
       return 0.0;
     });
     __syncwarp();
     if (lane == 0)
       s = pw_combine(n, [&](int64_t, int64_t, int64_t idx) { return scratch[idx]; });
   } else if (lane == 0) {
-    s = pw_combine(n, [&](int64_t start, int64_t len, int64_t) { return pw_leaf(a + start, len); });
+    s = pw_combine(n, [&](int64_t start, int64_t len, int64_t) {
+      return pw_leaf(a + start, len, sexp);
+    });
   }
   __syncwarp();
   return __shfl_sync(DSK_FULL, s, 0);

@@ -21,14 +21,18 @@
 // the next row's corner) and are skipped; the shared row r_lo is filtered on
 // the computed rank.  The union of the bands 1..phi equals the reference's
 // from-scratch recompute at phi (prefix property).
+//
+// Queue records are 16-byte words in structure-of-arrays layout so each
+// field group moves with one conflict-free LDS.128 / STS.128.
 #pragma once
 #include "dsk_device.cuh"
 
 namespace dsk {
 
-constexpr int kWarps = 16;   // warps per CTA (one CTA per SM)
+constexpr int kWarps = 24;   // warps per CTA (one CTA per SM)
 constexpr int kQ = 64;       // queue capacity per level
 constexpr int kJs = 64;      // folded (j, stream) table rows; Poisson counts < 64
+constexpr int kRwin = 128;   // per-pass rank-window table entries per warp
 
 struct SmemTables {
   uint64_t tE[8][256];    // T0..T7  element bytes
@@ -47,27 +51,16 @@ struct SmemTables {
 };
 
 struct WarpQueues {
-  // region queue
-  uint64_t rgP[kQ];
-  double rgX[kQ];
-  uint32_t rgWhi[kQ], rgRlo[kQ], rgRhi[kQ], rgMeta[kQ];
-  // area queue
-  uint64_t arP[kQ];
-  double arX[kQ];
-  uint32_t arW[kQ], arR[kQ], arMeta[kQ];
-  uint32_t arElem[kQ];
-  // hit queue
-  double htRank[kQ];
-  uint64_t htP[kQ];
-  uint32_t htJ[kQ];
-  // element chunk
-  uint64_t elE[32];
-  double elX[32];
+  ulonglong2 rgA[kQ];   // region: {P_R, x}
+  uint4 rgB[kQ];        //         {w_hi, r_lo, r_hi, meta}
+  ulonglong2 arA[kQ];   // area:   {P_A, x}
+  uint4 arB[kQ];        //         {w, r, meta, element index (materialising sink)}
+  ulonglong2 ht[kQ];    // hit:    {P_A ^ js[j][fp], rank bits}
+  ulonglong2 el[32];    // element chunk: {E, x}
   uint32_t elIdx[32];
-  uint32_t pad;
 };
 
-// region meta: nu | rho << 8 | flags << 16
+// region meta: nu | rho << 8 | flags << 16 (| element index << 19, materialising sink)
 constexpr uint32_t kRgHasPrev = 1u << 16, kRgWide = 1u << 17, kRgNarrow = 1u << 18;
 // area meta: nu | rho << 8 | count << 16 | flags << 24
 constexpr uint32_t kArWb = 1u << 24, kArRb = 1u << 25, kArLb = 1u << 26;
@@ -75,8 +68,11 @@ constexpr uint32_t kArWb = 1u << 24, kArRb = 1u << 25, kArLb = 1u << 26;
 struct PassParams {
   const uint64_t *gtab;  // global 22x256 tables (rare wide-key bytes)
   double inv_t;          // fl(1 / t)
+  double tf;             // t
   double L_hi, L_lo;     // band (L_lo < 0: first pass)
   int RD, RD_lo;         // rank depths of L_hi and L_lo
+  int maxd;              // max element depth of the set (rank-window table extent)
+  uint64_t pt0, pt1, pt2, pt3;  // first Poisson thresholds (registers)
 };
 
 // A hit that survived the rank/weight filters.
@@ -95,22 +91,58 @@ struct DartRow {
   uint64_t fp;
 };
 
+// Poisson(1) count: #{m : X >= thr[m]} (inverse CDF, ref/randomness.py:145-147);
+// counts >= 4 (2% of areas) finish in a loop over the shared table.
+__device__ __forceinline__ uint32_t poisson_count(uint64_t X, const PassParams &P,
+                                                  const SmemTables &T) {
+  uint32_t c = (X >= P.pt0) + (X >= P.pt1) + (X >= P.pt2) + (X >= P.pt3);
+  if (c == 4) {
+    while (X >= T.pthr[c]) c++;
+  }
+  return c;
+}
+
 template <class Sink, bool kFull>
 struct Engine {
   const SmemTables &T;
   WarpQueues &Q;
+  uint2 *rwin;          // per-pass rank windows by (nu, rho): {r_hi + 1, r_lo | hasprev << 31}
   Sink &sink;
-  const PassParams &P;
+  const PassParams P;
   int lane;
   int rg_head = 0, rg_cnt = 0, ar_head = 0, ar_cnt = 0, ht_head = 0, ht_cnt = 0;
-  // statistics
-  double warp_full = 0.0;   // warp-uniform: areas of the full (non-band) step (area cap)
-  bool abort = false;       // warp-uniform: area cap exceeded
+  bool use_table = false;
+  bool abort = false;       // warp-uniform: area cap exceeded by one lane's share
+  double lane_full = 0.0;   // per lane: areas of the full (non-band) step (area cap)
   uint32_t n_darts = 0;     // per lane: candidate darts first seen in this band
   uint32_t n_hits = 0;      // per lane
 
-  __device__ Engine(const SmemTables &t, WarpQueues &q, Sink &s, const PassParams &p, int ln)
-      : T(t), Q(q), sink(s), P(p), lane(ln) {}
+  __device__ Engine(const SmemTables &t, WarpQueues &q, uint2 *rw, Sink &s, const PassParams &p,
+                    int ln)
+      : T(t), Q(q), rwin(rw), sink(s), P(p), lane(ln) {
+    // rank windows depend on (nu, rho, limit) only: tabulate them per pass
+    const int rdp1 = P.RD + 1;
+    const int entries = (P.maxd + 1) * rdp1;
+    use_table = entries <= kRwin;
+    if (use_table) {
+      for (int e = lane; e < entries; e += 32) {
+        int nu = e / rdp1, rho = e - nu * rdp1;
+        double r0 = __dadd_rn(pow2(rho), -1.0);
+        double drho = pow2(rho - nu);
+        int64_t r_hi = rank_window(P.L_hi, nu, rho, r0, drho);
+        uint32_t lo = 0;
+        if (P.L_lo >= 0.0 && rho <= P.RD_lo) {
+          int64_t rp = rank_window(P.L_lo, nu, rho, r0, drho);
+          if (rp >= 0) lo = (uint32_t)rp | 0x80000000u;
+        }
+        // r_hi <= 2^27 whenever the step is legal; larger values saturate and
+        // the area cap rejects the step
+        uint32_t hi1 = r_hi < 0 ? 0u : (r_hi >= 0x7fffffff ? 0x7fffffffu : (uint32_t)r_hi + 1);
+        rwin[e] = make_uint2(hi1, lo);  // team warps write identical values
+      }
+    }
+    __syncwarp();
+  }
 
   // ---------------------------------------------------------------- hits
   __device__ void process_hits(int m) {
@@ -119,12 +151,11 @@ struct Engine {
     HitInfo h;
     h.rank = 0.0; h.fp = 0; h.bhash = 0;
     if (valid) {
-      h.rank = Q.htRank[idx];
-      uint64_t pa = Q.htP[idx];
-      uint32_t j = Q.htJ[idx];
-      h.fp = finalize(pa ^ T.js[j][kStreamFp - 1]);  // ref/randomness.py:149-152
+      ulonglong2 rec = Q.ht[idx];
+      h.rank = __longlong_as_double((long long)rec.y);
+      h.fp = finalize(rec.x);  // fingerprint, ref/randomness.py:149-152
       uint64_t f = h.fp;
-      uint64_t x = T.bconst;  // hash64(fp, stream=5), ref/randomness.py:154-158
+      uint64_t x = T.bconst;   // hash64(fp, stream=5), ref/randomness.py:154-158
 #pragma unroll
       for (int p = 0; p < 8; p++) x ^= T.tE[p][(f >> (8 * p)) & 0xff];
       h.bhash = finalize(x);
@@ -139,15 +170,12 @@ struct Engine {
     while (ht_cnt >= 32 || (force && ht_cnt > 0)) process_hits(ht_cnt < 32 ? ht_cnt : 32);
   }
 
-  __device__ void push_hit(bool valid, double rank, uint64_t pa, uint32_t j) {
+  __device__ void push_hit(bool valid, double rank, uint64_t fpkey) {
     unsigned b = __ballot_sync(DSK_FULL, valid);
     if (b == 0) return;
-    int off = __popc(b & ((1u << lane) - 1));
     if (valid) {
-      int idx = (ht_head + ht_cnt + off) & (kQ - 1);
-      Q.htRank[idx] = rank;
-      Q.htP[idx] = pa;
-      Q.htJ[idx] = j;
+      int idx = (ht_head + ht_cnt + __popc(b & ((1u << lane) - 1))) & (kQ - 1);
+      Q.ht[idx] = make_ulonglong2(fpkey, (unsigned long long)__double_as_longlong(rank));
     }
     ht_cnt += __popc(b);
     __syncwarp();
@@ -162,7 +190,7 @@ struct Engine {
     ar_head = (ar_head + m) & (kQ - 1);
     ar_cnt -= m;
     uint32_t c = 0;
-    if (lane < m) c = (Q.arMeta[(head + lane) & (kQ - 1)] >> 16) & 0xff;
+    if (lane < m) c = (Q.arB[(head + lane) & (kQ - 1)].z >> 16) & 0xff;
     uint32_t incl = warp_incl_scan(c, lane);
     uint32_t total = __shfl_sync(DSK_FULL, incl, 31);
     uint32_t excl = incl - c;
@@ -174,37 +202,38 @@ struct Engine {
       bool hit = false;
       double rank = 0.0, weight = 0.0;
       uint64_t pa = 0;
-      int ai = 0;
+      uint4 B = make_uint4(0, 0, 0, 0);
       if (valid) {
-        ai = (head + src) & (kQ - 1);
-        pa = Q.arP[ai];
-        uint32_t meta = Q.arMeta[ai];
+        int ai = (head + src) & (kQ - 1);
+        ulonglong2 A = Q.arA[ai];
+        B = Q.arB[ai];
+        pa = A.x;
+        uint32_t meta = B.z;
         int nu = meta & 0xff, rho = (meta >> 8) & 0xff;
-        uint32_t r = Q.arR[ai];
         // rank = r0 + (r + u) * drho, ref/darthash.py:282 (separately rounded)
         double u = u53(finalize(pa ^ T.js[j][kStreamU - 1]));
         double r0 = __dadd_rn(pow2(rho), -1.0);
-        rank = __dadd_rn(r0, __dmul_rn(__dadd_rn((double)r, u), pow2(rho - nu)));
+        rank = __dadd_rn(r0, __dmul_rn(__dadd_rn((double)B.y, u), pow2(rho - nu)));
         hit = true;
         if (meta & kArRb) hit = rank <= P.L_hi;        // interior rows pass by monotonicity
         if (meta & kArLb) hit = hit && rank > P.L_lo;  // band: exclude darts seen before
-        if (kFull || (hit && (meta & kArWb))) {  // only the w_hi column can miss
+        if (kFull || (hit && (meta & kArWb))) {        // only the w_hi column can miss
           double v = u53(finalize(pa ^ T.js[j][kStreamV - 1]));
           double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
           // weight = w0 + (w + v) * dnu, ref/darthash.py:281
-          weight = __dadd_rn(T.w0[nu], __dmul_rn(__dadd_rn((double)Q.arW[ai], v), dnu));
-          if (meta & kArWb) hit = hit && weight <= Q.arX[ai];  // ref/darthash.py:284
+          weight = __dadd_rn(T.w0[nu], __dmul_rn(__dadd_rn((double)B.x, v), dnu));
+          double x = __longlong_as_double((long long)A.y);
+          if (meta & kArWb) hit = hit && weight <= x;  // ref/darthash.py:284 (inclusive)
         }
       }
       if (kFull) {  // materialising sink: every hit with its full index tuple
         if (hit) {
-          uint32_t meta = Q.arMeta[ai];
           DartRow d;
-          d.elem = Q.arElem[ai];
-          d.nu = meta & 0xff;
-          d.rho = (meta >> 8) & 0xff;
-          d.w = Q.arW[ai];
-          d.r = Q.arR[ai];
+          d.elem = B.w;
+          d.nu = B.z & 0xff;
+          d.rho = (B.z >> 8) & 0xff;
+          d.w = B.x;
+          d.r = B.y;
           d.j = j;
           d.weight = weight;
           d.rank = rank;
@@ -213,7 +242,7 @@ struct Engine {
           n_hits++;
         }
       } else {
-        push_hit(hit, rank, pa, j);
+        push_hit(hit, rank, pa ^ T.js[j][kStreamFp - 1]);
       }
     }
   }
@@ -226,15 +255,10 @@ struct Engine {
                             uint32_t meta, uint32_t elem) {
     unsigned b = __ballot_sync(DSK_FULL, valid);
     if (b == 0) return;
-    int off = __popc(b & ((1u << lane) - 1));
     if (valid) {
-      int idx = (ar_head + ar_cnt + off) & (kQ - 1);
-      Q.arP[idx] = pa;
-      Q.arX[idx] = x;
-      Q.arW[idx] = w;
-      Q.arR[idx] = r;
-      Q.arMeta[idx] = meta;
-      if (kFull) Q.arElem[idx] = elem;
+      int idx = (ar_head + ar_cnt + __popc(b & ((1u << lane) - 1))) & (kQ - 1);
+      Q.arA[idx] = make_ulonglong2(pa, (unsigned long long)__double_as_longlong(x));
+      Q.arB[idx] = make_uint4(w, r, meta, elem);
     }
     ar_cnt += __popc(b);
     __syncwarp();
@@ -250,8 +274,8 @@ struct Engine {
     rg_cnt -= m;
     uint32_t c = 0;
     if (lane < m) {
-      int i = (head + lane) & (kQ - 1);
-      c = (Q.rgWhi[i] + 1) * (Q.rgRhi[i] - Q.rgRlo[i] + 1);
+      uint4 B = Q.rgB[(head + lane) & (kQ - 1)];
+      c = (B.x + 1) * (B.z - B.y + 1);
     }
     uint32_t incl = warp_incl_scan(c, lane);
     uint32_t total = __shfl_sync(DSK_FULL, incl, 31);
@@ -267,8 +291,9 @@ struct Engine {
       uint32_t w = 0, r = 0, meta = 0, elem = 0;
       if (valid) {
         int gi = (head + src) & (kQ - 1);
-        uint32_t whi = Q.rgWhi[gi], rlo = Q.rgRlo[gi], rhi = Q.rgRhi[gi];
-        uint32_t rmeta = Q.rgMeta[gi];
+        ulonglong2 A = Q.rgA[gi];
+        uint4 B = Q.rgB[gi];
+        uint32_t whi = B.x, rlo = B.y, rhi = B.z, rmeta = B.w;
         if (whi == 0) {
           w = 0;
           r = rlo + off;
@@ -277,7 +302,7 @@ struct Engine {
           w = off / rc;
           r = rlo + (off - w * rc);
         }
-        pa = Q.rgP[gi];
+        pa = A.x;
         if (rmeta & kRgNarrow) {
           pa ^= T.tW[0][w] ^ T.tR[0][r];
         } else {
@@ -290,16 +315,14 @@ struct Engine {
                   __ldg(&P.gtab[17 * 256 + (r >> 24)]);
         }
         // poisson1, ref/randomness.py:145-147 / :209-211 (j = 0, stream 3)
-        uint64_t X = finalize(pa ^ T.js[0][kStreamPoisson - 1]) >> 11;
-        uint32_t cnt = 0;
-        while (X >= T.pthr[cnt]) cnt++;
+        uint32_t cnt = poisson_count(finalize(pa ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
         bool lb = (rmeta & kRgHasPrev) && r == rlo;
         if (!lb) n_darts += cnt;
         keep = cnt > 0;
         meta = (rmeta & 0xffff) | (cnt << 16) | (w == whi ? kArWb : 0) | (r == rhi ? kArRb : 0) |
                (lb ? kArLb : 0);
-        x = Q.rgX[gi];
-        if (kFull) elem = Q.rgMeta[gi] >> 19;  // debug: element index stored in meta
+        x = __longlong_as_double((long long)A.y);
+        if (kFull) elem = rmeta >> 19;  // materialising sink: element index
       }
       push_area(keep, pa, x, w, r, meta, elem);
     }
@@ -313,15 +336,10 @@ struct Engine {
                               uint32_t rhi, uint32_t meta) {
     unsigned b = __ballot_sync(DSK_FULL, valid);
     if (b == 0) return;
-    int off = __popc(b & ((1u << lane) - 1));
     if (valid) {
-      int idx = (rg_head + rg_cnt + off) & (kQ - 1);
-      Q.rgP[idx] = pr;
-      Q.rgX[idx] = x;
-      Q.rgWhi[idx] = whi;
-      Q.rgRlo[idx] = rlo;
-      Q.rgRhi[idx] = rhi;
-      Q.rgMeta[idx] = meta;
+      int idx = (rg_head + rg_cnt + __popc(b & ((1u << lane) - 1))) & (kQ - 1);
+      Q.rgA[idx] = make_ulonglong2(pr, (unsigned long long)__double_as_longlong(x));
+      Q.rgB[idx] = make_uint4(whi, rlo, rhi, meta);
     }
     rg_cnt += __popc(b);
     __syncwarp();
@@ -331,7 +349,7 @@ struct Engine {
   // ------------------------------------------------------------- regions
   // One element chunk (<= 32 elements, lane i holds element i): expand each
   // element into its (nu, rho) regions and compute the surviving rectangle
-  // (ref/darthash.py:180-225).  Returns false when the area cap tripped.
+  // (ref/darthash.py:180-225).  Sets `abort` when the area cap trips.
   __device__ void element_chunk(bool valid, uint64_t id, double x, int depth, uint32_t eidx) {
     uint64_t E = 0;
     if (valid) {
@@ -339,11 +357,11 @@ struct Engine {
       for (int p = 0; p < 8; p++) E ^= T.tE[p][(id >> (8 * p)) & 0xff];
     }
     __syncwarp();
-    Q.elE[lane] = E;
-    Q.elX[lane] = x;
-    Q.elIdx[lane] = eidx;
+    Q.el[lane] = make_ulonglong2(E, (unsigned long long)__double_as_longlong(x));
+    if (kFull) Q.elIdx[lane] = eidx;
     __syncwarp();
     const int rdp1 = P.RD + 1;
+    const float inv_rdp1 = 1.0f / (float)rdp1;
     uint32_t c = valid ? (uint32_t)(depth + 1) * (uint32_t)rdp1 : 0;
     uint32_t incl = warp_incl_scan(c, lane);
     uint32_t total = __shfl_sync(DSK_FULL, incl, 31);
@@ -354,51 +372,62 @@ struct Engine {
       int src = warp_owner(excl, pos);
       uint32_t idx = pos - __shfl_sync(DSK_FULL, excl, src);
       uint64_t pr = 0;
-      double xs = 0.0, full = 0.0;
+      double xs = 0.0;
       uint32_t whi = 0, rlo = 0, rhi = 0, meta = 0;
       if (ok) {
         int nu, rho;
-        if (rdp1 == 1) { nu = (int)idx; rho = 0; }
-        else { nu = (int)(idx / (uint32_t)rdp1); rho = (int)(idx - (uint32_t)nu * rdp1); }
-        xs = Q.elX[src];
-        double r0 = __dadd_rn(pow2(rho), -1.0);
-        double drho = pow2(rho - nu);
-        int64_t r_hi = rank_window(P.L_hi, nu, rho, r0, drho);
-        int64_t w_hi = -1;
-        if (r_hi >= 0) {
-          double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
-          w_hi = weight_window(xs, T.w0[nu], dnu, rho);
+        if (rdp1 == 1) {
+          nu = (int)idx;
+          rho = 0;
+        } else {  // fp32 quotient, off by at most one: corrected below
+          nu = (int)(((float)idx + 0.5f) * inv_rdp1);
+          rho = (int)idx - nu * rdp1;
+          if (rho < 0) { nu--; rho += rdp1; }
+          else if (rho >= rdp1) { nu++; rho -= rdp1; }
         }
-        if (w_hi >= 0) {
-          full = (double)(w_hi + 1) * (double)(r_hi + 1);
-          int64_t r_lo = 0;
-          uint32_t flags = 0;
+        ulonglong2 el = Q.el[src];
+        xs = __longlong_as_double((long long)el.y);
+        int64_t r_hi, r_lo = 0;
+        uint32_t flags = 0;
+        if (use_table) {
+          uint2 rw = rwin[nu * rdp1 + rho];
+          r_hi = (int64_t)rw.x - 1;
+          if (rw.y & 0x80000000u) { r_lo = rw.y & 0x7fffffffu; flags |= kRgHasPrev >> 16; }
+        } else {
+          double r0 = __dadd_rn(pow2(rho), -1.0);
+          double drho = pow2(rho - nu);
+          r_hi = rank_window(P.L_hi, nu, rho, r0, drho);
           if (P.L_lo >= 0.0 && rho <= P.RD_lo) {
             int64_t rp = rank_window(P.L_lo, nu, rho, r0, drho);
             if (rp >= 0) { r_lo = rp; flags |= kRgHasPrev >> 16; }
           }
-          ok = r_lo <= r_hi;
-          if (ok) {
-            whi = (uint32_t)w_hi; rlo = (uint32_t)r_lo; rhi = (uint32_t)r_hi;
-            uint64_t E2 = Q.elE[src];
-            pr = E2 ^ T.tNu[nu] ^ T.tRho[rho];
-            if (w_hi >= 65536 || r_hi >= 65536) flags |= kRgWide >> 16;
-            else pr ^= T.cfold;
-            if (w_hi < 256 && r_hi < 256) { flags |= kRgNarrow >> 16; pr ^= T.nfold; }
-            meta = (uint32_t)nu | ((uint32_t)rho << 8) | (flags << 16);
-            if (kFull) meta |= Q.elIdx[src] << 19;
-          }
-        } else {
-          ok = false;
+        }
+        int64_t w_hi = -1;
+        if (r_hi >= 0) {
+          double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
+          w_hi = weight_window(xs, T.w0[nu], dnu, __dmul_rn(P.tf, pow2(rho - nu)), rho);
+        }
+        ok = w_hi >= 0 && r_lo <= r_hi;
+        if (w_hi >= 0) {
+          double full = (double)(w_hi + 1) * (double)(r_hi + 1);
+          lane_full += full;
+          // a region over the cap makes the step illegal (ref/darthash.py:242-244)
+          if (full > kMaxAreas) ok = false;
+        }
+        if (ok) {
+          whi = (uint32_t)w_hi; rlo = (uint32_t)r_lo; rhi = (uint32_t)r_hi;
+          pr = el.x ^ T.tNu[nu] ^ T.tRho[rho];
+          if (w_hi >= 65536 || r_hi >= 65536) flags |= kRgWide >> 16;
+          else pr ^= T.cfold;
+          if (w_hi < 256 && r_hi < 256) { flags |= kRgNarrow >> 16; pr ^= T.nfold; }
+          meta = (uint32_t)nu | ((uint32_t)rho << 8) | (flags << 16);
+          if (kFull) meta |= Q.elIdx[src] << 19;
         }
       }
-      // Area cap (ref/darthash.py:242-244), accumulated before anything of
-      // this batch is queued: every queued batch then totals <= 2^27 areas.
-      double bsum = full;
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) bsum += __shfl_xor_sync(DSK_FULL, bsum, o);
-      warp_full += bsum;
-      if (warp_full > kMaxAreas) { abort = true; return; }
+      // Any lane whose share exceeds the cap proves the step illegal; the exact
+      // team-wide sum is checked after the pass.  Every queued region then
+      // holds <= 2^27 areas.
+      if (__any_sync(DSK_FULL, lane_full > kMaxAreas)) { abort = true; return; }
       push_region(ok, pr, xs, whi, rlo, rhi, meta);
     }
   }
@@ -407,6 +436,13 @@ struct Engine {
     drain_regions(true);
     drain_areas(true);
     drain_hits(true);
+  }
+
+  __device__ double warp_full() const {
+    double s = lane_full;
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(DSK_FULL, s, o);
+    return s;
   }
 };
 

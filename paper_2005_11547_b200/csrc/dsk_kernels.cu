@@ -3,7 +3,7 @@
 //   K1+K2+K3+K4  minhash_kernel   CSR ingest, l1, validation, DartHash
 //                                 enumeration, k-slot (rank, index) minimum,
 //                                 in-kernel phi-band retry, 1-bit epilogue
-//   K5           lsh_kernel       (dsk_lsh.cuh) bottom-K per table + mix64
+//   K5           lsh_kernel       (dsk_lsh_kernel.cuh) bottom-K per table + mix64
 //   K6           darts_kernel     DartBatch materialisation (tests)
 //   K0           hash_peak_kernel hash-rate microbenchmark (roofline peak)
 //   utilities    hash64 / mix64 / pack_onebit kernels
@@ -45,6 +45,10 @@ struct dsk_ctx {
   size_t stage_bytes = 0;
   cudaStream_t hs[2] = {nullptr, nullptr};
   cudaEvent_t ev_in[2] = {nullptr, nullptr};
+  // LSH hit buffers (one slice per resident team)
+  std::mutex scratch_mu;
+  void *lsh_scratch = nullptr;
+  size_t lsh_scratch_bytes = 0;
 };
 
 constexpr int kCounterSlots = 256;
@@ -127,9 +131,15 @@ struct TeamCtl {
   int maxdepth;
   unsigned int darts;
   unsigned int hits;
-  int pad[3];
+  int sexp;       // weight rescaling exponent (LSH normalisation), 0 otherwise
+  unsigned int total;  // LSH: buffered hits
+  int overflow;        // LSH: hit buffer overflow
 };
-constexpr size_t kTeamCtlBytes = align16(sizeof(TeamCtl));
+// per-team block: control word + the per-pass rank-window table
+constexpr size_t kTeamCtlBytes = align16(sizeof(TeamCtl)) + kRwin * sizeof(uint2);
+__device__ __forceinline__ uint2 *team_rwin(TeamCtl *C) {
+  return reinterpret_cast<uint2 *>(reinterpret_cast<unsigned char *>(C) + align16(sizeof(TeamCtl)));
+}
 
 __device__ __forceinline__ void team_sync(int G, int team) {
   if (G == 1) {
@@ -207,39 +217,54 @@ struct MinhashArgs {
 
 // Per-set validation and l1 by warp 0 of the team: empty set (ref/sketching.py:86-88),
 // finite positive weights (ref/core.py:38-41), l1 = np.sum (ref/core.py:44),
-// max element depth (ref/darthash.py:154-158).
-__device__ void set_prologue(const MinhashArgs &a, const SmemTables &T, TeamCtl &C, int64_t lo,
-                             int64_t nnz, double *scratch, int lane) {
+// max element depth (ref/darthash.py:154-158).  With `normalize`, the set is
+// first rescaled by 2^-weight_class(l1) as LshIndex.insert does
+// (ref/annindex.py:130-131, ref/core.py:57-60): C.sexp = -c and l1 is the
+// np.sum of the rescaled weights.
+__device__ void set_prologue(const double *w, double tf, const SmemTables &T, TeamCtl &C,
+                             int64_t lo, int64_t nnz, double *scratch, int lane, bool normalize) {
   if (nnz == 0) {
     if (lane == 0) C.status = DSK_EMPTY;
     return;
   }
   bool bad = false;
-  int maxd = 0;
   for (int64_t i = lane; i < nnz; i += 32) {
-    double x = a.w[lo + i];
+    double x = w[lo + i];
     bad |= !(isfinite(x) && x > 0.0);
-    int d = floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, x)), T.l2thr);
-    maxd = d > maxd ? d : maxd;
   }
   bad = __any_sync(DSK_FULL, bad);
+  double l1 = warp_np_sum(w + lo, nnz, scratch, lane, 0);
+  int sexp = 0;
+  if (normalize && !bad) {
+    int e;
+    frexp(l1, &e);  // weight_class, ref/annindex.py:39-44
+    sexp = -(e - 1);
+    l1 = warp_np_sum(w + lo, nnz, scratch, lane, sexp);
+  }
+  int maxd = 0;
+  for (int64_t i = lane; i < nnz; i += 32) {
+    double x = sexp ? scalbn(w[lo + i], sexp) : w[lo + i];
+    int d = floor_log2_host(__dadd_rn(1.0, __dmul_rn(tf, x)), T.l2thr);
+    maxd = d > maxd ? d : maxd;
+  }
   maxd = __reduce_max_sync(DSK_FULL, (unsigned)maxd);
-  double l1 = warp_np_sum(a.w + lo, nnz, scratch, lane);
   if (lane == 0) {
     C.l1 = l1;
     C.maxdepth = maxd;
+    C.sexp = sexp;
     if (bad) C.status = DSK_WEIGHT;
   }
 }
 
 template <class Sink>
 __device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const PassParams &P,
-                         const int64_t *indptr_unused, const uint64_t *ids, const double *w,
-                         int64_t lo, int64_t nnz, int G, int wit, int lane, double tf,
-                         TeamCtl &C, uint32_t &n_darts, uint32_t &n_hits) {
-  (void)indptr_unused;
-  Engine<Sink, false> eng(T, Q, sink, P, lane);
-  const int CH = 32 / G;
+                         const uint64_t *ids, const double *w, int64_t lo, int64_t nnz, int G,
+                         int wit, int lane, double tf, TeamCtl &C, uint32_t &n_darts,
+                         uint32_t &n_hits, int sexp = 0) {
+  Engine<Sink, false> eng(T, Q, team_rwin(&C), sink, P, lane);
+  // element chunks go round-robin to the team's warps; small sets use
+  // narrower chunks so every warp of the team gets elements
+  const int CH = (G == 1 || nnz >= 64 * G) ? 32 : (32 / G > 4 ? 32 / G : 4);
   for (int64_t c = wit; c * CH < nnz; c += G) {
     int64_t e = c * CH + lane;
     bool valid = lane < CH && e < nnz;
@@ -249,6 +274,7 @@ __device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const P
     if (valid) {
       id = ids[lo + e];
       x = w[lo + e];
+      if (sexp) x = scalbn(x, sexp);
       depth = floor_log2_host(__dadd_rn(1.0, __dmul_rn(tf, x)), T.l2thr);
     }
     eng.element_chunk(valid, id, x, depth, (uint32_t)e);
@@ -257,10 +283,18 @@ __device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const P
   if (!eng.abort) eng.finish();
   n_darts += eng.n_darts;
   n_hits += eng.n_hits;
+  double wf = eng.warp_full();
   if (lane == 0) {
-    atomicAdd(&C.areas, eng.warp_full);
+    atomicAdd(&C.areas, wf);
     if (eng.abort) atomicOr(&C.abort, 1);
   }
+}
+
+__device__ __forceinline__ void poisson_regs(PassParams &P, const SmemTables &T) {
+  P.pt0 = T.pthr[0];
+  P.pt1 = T.pthr[1];
+  P.pt2 = T.pthr[2];
+  P.pt3 = T.pthr[3];
 }
 
 __global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) {
@@ -298,7 +332,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) 
       C.darts = 0; C.hits = 0;
     }
     team_sync(G, team);
-    if (wit == 0) set_prologue(a, T, C, lo, nnz, reinterpret_cast<double *>(&Q), lane);
+    if (wit == 0)
+      set_prologue(a.w, a.tf, T, C, lo, nnz, reinterpret_cast<double *>(&Q), lane, false);
     team_sync(G, team);
     int status = C.status;
     int phi_star = 0;
@@ -320,12 +355,14 @@ __global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) 
         PassParams P;
         P.gtab = a.tabs.tab;
         P.inv_t = a.inv_t;
+        P.tf = a.tf;
         P.L_hi = L;
         P.L_lo = L_prev;
         P.RD = RD;
         P.RD_lo = RD_prev;
-        run_pass(T, Q, sink, P, a.indptr, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts,
-                 n_hits);
+        P.maxd = maxd;
+        poisson_regs(P, T);
+        run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits);
         team_sync(G, team);
         const double areas = C.areas;
         const bool ab = C.abort != 0;
@@ -433,6 +470,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
   unsigned long long *cursors =
       reinterpret_cast<unsigned long long *>(smem + kOffTeam);
+  uint2 *rwin = reinterpret_cast<uint2 *>(smem + kOffTeam + kWarps * sizeof(unsigned long long)) +
+                warp * kRwin;
   __syncthreads();
   for (int64_t s = (int64_t)blockIdx.x * kWarps + warp; s < a.n; s += (int64_t)gridDim.x * kWarps) {
     const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
@@ -454,10 +493,13 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
       PassParams P;
       P.gtab = a.tabs.tab;
       P.inv_t = a.inv_t;
+      P.tf = a.tf;
       P.L_hi = L;
       P.L_lo = -1.0;
       P.RD = RD;
       P.RD_lo = 0;
+      P.maxd = maxd;
+      poisson_regs(P, T);
       RowSink sink;
       sink.a = &a;
       sink.set = s;
@@ -465,7 +507,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
       sink.cursor = &cursors[warp];
       // the area cap is checked on a counting pass first (ref/darthash.py:242-244
       // raises before any dart is produced)
-      Engine<RowSink, true> eng(T, Q, sink, P, lane);
+      Engine<RowSink, true> eng(T, Q, rwin, sink, P, lane);
       for (int64_t c = 0; c * 32 < nnz; c++) {
         int64_t e = c * 32 + lane;
         bool valid = e < nnz;
@@ -560,6 +602,8 @@ __global__ void __launch_bounds__(512) hash_peak_kernel(const uint64_t *tab, int
   if (x == 0x9e3779b97f4a7c15ULL) sink[0] = x;  // practically never; keeps the work live
 }
 
+#include "dsk_lsh_kernel.cuh"
+
 // ------------------------------------------------------------- host side
 
 static size_t minhash_smem(int k, int G) {
@@ -595,6 +639,8 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(darts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
   *out = c;
   return DSK_OK;
 }
@@ -607,6 +653,7 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
   cudaFree(c->d_l2thr);
   cudaFree(c->d_counter);
   if (c->stage) cudaFree(c->stage);
+  if (c->lsh_scratch) cudaFree(c->lsh_scratch);
   for (int i = 0; i < 2; i++) {
     if (c->hs[i]) cudaStreamDestroy(c->hs[i]);
     if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
@@ -626,10 +673,10 @@ static TableArgs table_args(const dsk_ctx *c, double tf) {
   return t;
 }
 
+// smallest team (warps per set) whose slot arrays fit beside the queues
 static int choose_team(const dsk_ctx *c, int k) {
-  for (int G = 1; G <= kWarps; G *= 2)
-    if (minhash_smem(k, G) <= c->max_smem && (size_t)(kWarps / G) * k * 16 <= 96 * 1024) return G;
-  for (int G = 1; G <= kWarps; G *= 2)
+  static const int kTeams[] = {1, 2, 3, 4, 6, 8, 12, 24};
+  for (int G : kTeams)
     if (minhash_smem(k, G) <= c->max_smem) return G;
   return -1;
 }
@@ -685,7 +732,7 @@ extern "C" int dsk_darts_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *
   a.counts = counts; a.status = status; a.element = element; a.nu = nu; a.rho = rho; a.ww = w;
   a.rr = r; a.jj = j; a.weight = weight; a.rank = rank; a.fp = fingerprint;
   a.tabs = table_args(c, (double)t);
-  size_t smem = kOffTeam + kWarps * sizeof(unsigned long long);
+  size_t smem = kOffTeam + kWarps * (sizeof(unsigned long long) + kRwin * sizeof(uint2));
   int grid = (int)((n + kWarps - 1) / kWarps);
   if (grid > c->num_sms) grid = c->num_sms;
   darts_kernel<<<grid, kWarps * 32, smem, st>>>(a);
@@ -851,4 +898,4 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
   return DSK_OK;
 }
 
-#include "dsk_lsh.cuh"
+#include "dsk_lsh_host.cuh"

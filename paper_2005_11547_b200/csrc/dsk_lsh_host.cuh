@@ -1,0 +1,96 @@
+// dsk_lsh_host.cuh -- host side of K5 (included at the end of dsk_kernels.cu).
+
+static int choose_lsh_team(const dsk_ctx *c, int L) {
+  static const int kTeams[] = {1, 2, 3, 4, 6, 8, 12, 24};
+  for (int G : kTeams)
+    if (lsh_smem(L, G) <= c->max_smem) return G;
+  return -1;
+}
+
+extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
+                           const double *weights, int64_t n, int32_t L, int32_t K,
+                           int32_t normalize, uint64_t *out_keys, uint64_t *out_fps,
+                           int32_t *status, int32_t *phi, uint32_t *stats, void *stream) {
+  if (!c || !indptr || !status || n < 0) return set_err(DSK_EARG, "bad argument");
+  if (L < 1 || K < 1) return set_err(DSK_EARG, "L and K must be positive");  // ref/annindex.py:33-34
+  if (n == 0) return DSK_OK;
+  int64_t t = (int64_t)L * K;
+  if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "L*K too large");
+  int G = choose_lsh_team(c, L);
+  if (G < 0) return set_err(DSK_EUNSUPPORTED, "L too large for the shared-memory bucket counters");
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(c->device));
+  const int teams = kWarps / G;
+  int grid = c->num_sms;
+  if ((int64_t)grid * teams > n) grid = (int)((n + teams - 1) / teams);
+  // hit buffer per team: ~8 phi steps of L*K darts, at least 16K entries
+  uint32_t cap = (uint32_t)(8 * t > 16384 ? 8 * t : 16384);
+  size_t team_bytes = align16((size_t)cap * 24) + align16((size_t)L * K * 8);
+  size_t need = (size_t)grid * teams * team_bytes;
+  {
+    std::lock_guard<std::mutex> lock(c->scratch_mu);
+    if (c->lsh_scratch_bytes < need) {
+      if (c->lsh_scratch) CUDA_TRY(cudaFree(c->lsh_scratch));
+      c->lsh_scratch = nullptr;
+      c->lsh_scratch_bytes = 0;
+      CUDA_TRY(cudaMalloc(&c->lsh_scratch, need));
+      c->lsh_scratch_bytes = need;
+    }
+  }
+  unsigned long long *counter = c->d_counter + (c->next_slot.fetch_add(1) % kCounterSlots);
+  CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
+  LshArgs a;
+  a.indptr = indptr; a.ids = ids; a.w = weights; a.n = n; a.L = L; a.K = K;
+  a.normalize = normalize; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
+  a.md = make_mod((uint32_t)L); a.G = G; a.out_keys = out_keys; a.out_fps = out_fps;
+  a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
+  a.scratch = (unsigned char *)c->lsh_scratch; a.team_scratch = team_bytes; a.cap = cap;
+  a.tabs = table_args(c, (double)t);
+  lsh_kernel<<<grid, kWarps * 32, lsh_smem(L, G), st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}
+
+extern "C" int dsk_lsh_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
+                                const double *weights, int64_t n, int32_t L, int32_t K,
+                                int32_t normalize, uint64_t *out_keys, uint64_t *out_fps,
+                                int32_t *status, int32_t *phi, uint32_t *stats) {
+  if (!c || !indptr || !status || n < 0 || L < 1 || K < 1) return set_err(DSK_EARG, "bad argument");
+  if (n == 0) return DSK_OK;
+  if (indptr[0] != 0) return set_err(DSK_EARG, "indptr[0] must be 0");
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lock(c->host_mu);
+  const int64_t nnz = indptr[n];
+  size_t off_i = align16((n + 1) * 8), off_w = off_i + align16(nnz * 8);
+  size_t off_k = off_w + align16(nnz * 8);
+  size_t off_f = off_k + (out_keys ? align16((size_t)n * L * 8) : 0);
+  size_t off_s = off_f + (out_fps ? align16((size_t)n * L * K * 8) : 0);
+  size_t off_ph = off_s + align16(n * 4);
+  size_t off_st = off_ph + (phi ? align16(n * 4) : 0);
+  size_t total = off_st + (stats ? align16(n * 16) : 0);
+  int rc = ensure_stage(c, total);
+  if (rc) return rc;
+  char *base = (char *)c->stage;
+  int64_t *dp = (int64_t *)base;
+  uint64_t *di = (uint64_t *)(base + off_i);
+  double *dw = (double *)(base + off_w);
+  uint64_t *dk = out_keys ? (uint64_t *)(base + off_k) : nullptr;
+  uint64_t *df = out_fps ? (uint64_t *)(base + off_f) : nullptr;
+  int32_t *ds = (int32_t *)(base + off_s);
+  int32_t *dph = phi ? (int32_t *)(base + off_ph) : nullptr;
+  uint32_t *dst = stats ? (uint32_t *)(base + off_st) : nullptr;
+  cudaStream_t st = c->hs[0];
+  CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(di, ids, nnz * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(dw, weights, nnz * 8, cudaMemcpyHostToDevice, st));
+  rc = dsk_lsh_csr(c, dp, di, dw, n, L, K, normalize, dk, df, ds, dph, dst, st);
+  if (rc) return rc;
+  if (out_keys) CUDA_TRY(cudaMemcpyAsync(out_keys, dk, (size_t)n * L * 8, cudaMemcpyDeviceToHost, st));
+  if (out_fps)
+    CUDA_TRY(cudaMemcpyAsync(out_fps, df, (size_t)n * L * K * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(status, ds, n * 4, cudaMemcpyDeviceToHost, st));
+  if (phi) CUDA_TRY(cudaMemcpyAsync(phi, dph, n * 4, cudaMemcpyDeviceToHost, st));
+  if (stats) CUDA_TRY(cudaMemcpyAsync(stats, dst, n * 16, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return DSK_OK;
+}

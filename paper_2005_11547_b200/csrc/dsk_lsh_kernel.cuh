@@ -1,0 +1,272 @@
+// dsk_lsh_kernel.cuh -- K5: (L, K) LSH table keys (included by dsk_kernels.cu).
+//
+// lsh_key (ref/annindex.py:64-82): density t = L*K; darts are bucketed by
+// hash64(fp, stream 5) mod L; at the first phi step where every bucket holds
+// >= K darts (and >= L*K darts in total), each table's key is the K
+// smallest darts of its bucket by (rank, index), in order.  LshIndex folds
+// each key with HashFamily.mix64 (ref/annindex.py:135, ref/randomness.py:
+// 160-166); that fold is fused here as the epilogue.
+//
+// Per team (G warps on one set):
+//   enumeration  the shared engine, phi bands 1, 2, ... as for minhash; the
+//                sink appends every hit {rank, fp} to a global per-team
+//                scratch (L2-resident) and counts hits per bucket in smem;
+//   check        after each band: all L buckets >= K (counter of buckets
+//                that reached K);
+//   selection    counting sort of the buffered hits by bucket, then for each
+//                bucket the position of every entry among its bucket by
+//                (rank bits, fp) -- positions < K are the key, in order;
+//   epilogue     one lane per table folds the K fingerprints with mix64.
+
+struct LshSink {
+  ulonglong2 *buf;      // global: {fp, rank bits} per buffered hit
+  uint32_t *bkt;        // global: bucket per buffered hit
+  uint32_t cap;
+  ModU32 md;
+  uint32_t K;
+  unsigned int *total;  // smem: buffered hits
+  unsigned int *cnt;    // smem: hits per bucket
+  unsigned int *full;   // smem: buckets holding >= K hits
+  int *overflow;
+
+  __device__ void hit(bool valid, const HitInfo &h, int lane) {
+    unsigned b = __ballot_sync(DSK_FULL, valid);
+    if (b == 0) return;
+    unsigned base = 0;
+    if (lane == 0) base = atomicAdd(total, (unsigned)__popc(b));
+    base = __shfl_sync(DSK_FULL, base, 0);
+    if (valid) {
+      uint32_t idx = base + __popc(b & ((1u << lane) - 1));
+      uint32_t bucket = mod_u32(h.bhash, md);
+      if (idx < cap) {
+        buf[idx] = make_ulonglong2(h.fp, (unsigned long long)__double_as_longlong(h.rank));
+        bkt[idx] = bucket;
+      } else {
+        atomicOr(overflow, 1);
+      }
+      if (atomicAdd(&cnt[bucket], 1u) == K - 1) atomicAdd(full, 1u);
+    }
+  }
+  __device__ void row(const DartRow &) {}
+};
+
+struct LshArgs {
+  const int64_t *indptr;
+  const uint64_t *ids;
+  const double *w;
+  int64_t n;
+  int32_t L, K;
+  int32_t normalize;
+  double tf, inv_t;
+  ModU32 md;
+  int G;
+  uint64_t *out_keys;
+  uint64_t *out_fps;
+  int32_t *status;
+  int32_t *phi;
+  uint32_t *stats;
+  unsigned long long *counter;
+  unsigned char *scratch;  // per-team global scratch
+  size_t team_scratch;     // bytes per team
+  uint32_t cap;            // buffered-hit capacity per team
+  TableArgs tabs;
+};
+
+constexpr int DSK_SCRATCH = 7;  // per-set status: hit buffer overflow
+
+__host__ __device__ inline size_t lsh_team_bytes(int L) {
+  return kTeamCtlBytes + align16((size_t)3 * L * sizeof(unsigned int)) + 16;
+}
+
+__host__ __device__ inline size_t lsh_smem(int L, int G) {
+  int teams = kWarps / G;
+  return kOffTeam + (size_t)teams * lsh_team_bytes(L);
+}
+
+__global__ void __launch_bounds__(kWarps * 32, 1) lsh_kernel(LshArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
+  load_tables(T, a.tabs);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.G, team = warp / G, wit = warp % G, tt = wit * 32 + lane;
+  const int L = a.L, K = a.K;
+  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
+  unsigned char *tb = smem + kOffTeam + team * lsh_team_bytes(L);
+  TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
+  unsigned int *cnt = reinterpret_cast<unsigned int *>(tb + kTeamCtlBytes);
+  unsigned int *off = cnt + L;
+  unsigned int *cur = off + L;
+  unsigned int *fullc = reinterpret_cast<unsigned int *>(tb + kTeamCtlBytes +
+                                                         align16((size_t)3 * L * sizeof(unsigned)));
+  // global scratch of this team
+  const int teams = kWarps / G;
+  unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
+  ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
+  uint32_t *bkt = reinterpret_cast<uint32_t *>(gs + (size_t)a.cap * 16);
+  uint32_t *order = bkt + a.cap;
+  uint64_t *sel = reinterpret_cast<uint64_t *>(gs + align16((size_t)a.cap * 24));
+  __syncthreads();
+
+  LshSink sink;
+  sink.buf = buf;
+  sink.bkt = bkt;
+  sink.cap = a.cap;
+  sink.md = a.md;
+  sink.K = (uint32_t)K;
+  sink.total = &C.total;
+  sink.cnt = cnt;
+  sink.full = fullc;
+  sink.overflow = &C.overflow;
+
+  for (;;) {
+    if (tt == 0) C.set = (long long)atomicAdd(a.counter, 1ULL);
+    team_sync(G, team);
+    const long long s = C.set;
+    if (s >= a.n) break;
+    const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
+    for (int i = tt; i < L; i += G * 32) cnt[i] = 0;
+    if (tt == 0) {
+      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0; C.areas = 0.0;
+      C.darts = 0; C.hits = 0; C.total = 0; C.sexp = 0; C.overflow = 0; *fullc = 0;
+    }
+    team_sync(G, team);
+    if (wit == 0)
+      set_prologue(a.w, a.tf, T, C, lo, nnz, reinterpret_cast<double *>(&Q), lane,
+                   a.normalize != 0);
+    team_sync(G, team);
+    int status = C.status;
+    int phi_star = 0;
+    double final_areas = 0.0;
+    uint32_t n_darts = 0, n_hits = 0;
+    if (status == 0) {
+      const double l1 = C.l1;
+      const int maxd = C.maxdepth;
+      const int sexp = C.sexp;
+      status = DSK_NOCONV;
+      double L_prev = -1.0;
+      int RD_prev = 0;
+      for (int phi = 1; phi <= 64; phi++) {  // ref/annindex.py:70
+        double Lim = __ddiv_rn((double)phi, l1);
+        if (!(Lim > 0.0) || isinf(Lim)) { status = DSK_LIMIT; break; }
+        int RD = floor_log2_host(__dadd_rn(1.0, Lim), T.l2thr);
+        if (maxd > 255 || RD > 255) { status = DSK_DEPTH; break; }
+        PassParams P;
+        P.gtab = a.tabs.tab;
+        P.inv_t = a.inv_t;
+        P.tf = a.tf;
+        P.L_hi = Lim;
+        P.L_lo = L_prev;
+        P.RD = RD;
+        P.RD_lo = RD_prev;
+        P.maxd = maxd;
+        poisson_regs(P, T);
+        run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
+                 sexp);
+        team_sync(G, team);
+        const double areas = C.areas;
+        const bool ab = C.abort != 0;
+        const unsigned total = C.total;
+        const unsigned full = *fullc;
+        const bool ovf = C.overflow != 0;
+        team_sync(G, team);
+        if (tt == 0) C.areas = 0.0;
+        if (ab || areas > kMaxAreas) { status = DSK_AREAS; break; }  // ref/darthash.py:243
+        if (ovf) { status = DSK_SCRATCH; break; }
+        final_areas = areas;
+        // ref/annindex.py:72-76: >= L*K darts and every bucket >= K
+        if (total >= (unsigned)(L * K) && full == (unsigned)L) {
+          status = DSK_OK;
+          phi_star = phi;
+          break;
+        }
+        L_prev = Lim;
+        RD_prev = RD;
+      }
+    }
+    unsigned wd = __reduce_add_sync(DSK_FULL, n_darts), wh = __reduce_add_sync(DSK_FULL, n_hits);
+    if (lane == 0) { atomicAdd(&C.darts, wd); atomicAdd(&C.hits, wh); }
+    team_sync(G, team);
+    if (status == 0) {
+      // ---- selection: counting sort by bucket (ref/annindex.py:77-81)
+      const unsigned total = C.total;
+      if (wit == 0) {  // exclusive scan of the bucket counts
+        unsigned carry = 0;
+        for (int b0 = 0; b0 < L; b0 += 32) {
+          unsigned v = b0 + lane < L ? cnt[b0 + lane] : 0;
+          unsigned incl = warp_incl_scan(v, lane);
+          if (b0 + lane < L) { off[b0 + lane] = carry + incl - v; cur[b0 + lane] = 0; }
+          carry += __shfl_sync(DSK_FULL, incl, 31);
+        }
+      }
+      team_sync(G, team);
+      for (unsigned i = tt; i < total; i += G * 32) {
+        uint32_t b = bkt[i];
+        order[off[b] + atomicAdd(&cur[b], 1u)] = i;
+      }
+      __threadfence_block();
+      team_sync(G, team);
+      // position of each entry within its bucket by (rank bits, fp); the
+      // buffer index breaks exact ties deterministically and flags them
+      bool tie = false;
+      for (int b = wit; b < L; b += G) {
+        const unsigned o = off[b], nb = cnt[b];
+        for (unsigned i = lane; i < nb; i += 32) {
+          uint32_t ei = order[o + i];
+          ulonglong2 e = buf[ei];
+          unsigned pos = 0;
+          for (unsigned m = 0; m < nb; m++) {
+            uint32_t mi = order[o + m];
+            ulonglong2 f = buf[mi];
+            bool less = f.y < e.y || (f.y == e.y && (f.x < e.x || (f.x == e.x && mi < ei)));
+            pos += less;
+            if (f.y == e.y && mi != ei && f.x != e.x) tie = true;
+          }
+          if (pos < (unsigned)K) sel[(size_t)b * K + pos] = e.x;
+        }
+      }
+      if (__any_sync(DSK_FULL, tie) && lane == 0) atomicOr(&C.tie, 1);
+      __threadfence_block();
+      team_sync(G, team);
+      // ---- epilogue: mix64 per table (ref/randomness.py:160-166)
+      for (int b = tt; b < L; b += G * 32) {
+        uint64_t mixed = 0;
+        for (int p = 0; p < K; p++) {
+          uint64_t v = sel[(size_t)b * K + p];
+          if (a.out_fps) a.out_fps[((size_t)s * L + b) * K + p] = v;
+          uint64_t e = v ^ mixed;
+          uint64_t h = 0;
+#pragma unroll
+          for (int q = 0; q < 8; q++) h ^= T.tE[q][(e >> (8 * q)) & 0xff];
+          // key fields other than element: w = p (T10, T11), stream 12
+          h ^= T.tNu[0] ^ T.tRho[0] ^ T.tW[0][p & 0xff] ^ T.tW[1][(p >> 8) & 0xff] ^
+               __ldg(&a.tabs.tab[12 * 256]) ^ __ldg(&a.tabs.tab[13 * 256]) ^ T.tR[0][0] ^
+               T.tR[1][0] ^ __ldg(&a.tabs.tab[16 * 256]) ^ __ldg(&a.tabs.tab[17 * 256]) ^
+               __ldg(&a.tabs.tab[18 * 256]) ^ __ldg(&a.tabs.tab[19 * 256]) ^
+               __ldg(&a.tabs.tab[20 * 256 + kStreamKeyMix]) ^ __ldg(&a.tabs.tab[21 * 256]);
+          mixed = finalize(h);
+        }
+        if (a.out_keys) a.out_keys[(size_t)s * L + b] = mixed;
+      }
+    } else {
+      for (int b = tt; b < L; b += G * 32) {
+        if (a.out_keys) a.out_keys[(size_t)s * L + b] = 0;
+        if (a.out_fps)
+          for (int p = 0; p < K; p++) a.out_fps[((size_t)s * L + b) * K + p] = 0;
+      }
+    }
+    team_sync(G, team);
+    if (tt == 0) {
+      a.status[s] = status | (C.tie ? DSK_STATUS_TIE : 0);
+      if (a.phi) a.phi[s] = phi_star;
+      if (a.stats) {
+        uint32_t *st = a.stats + (size_t)s * 4;
+        st[0] = (uint32_t)fmin(final_areas, 4294967295.0);
+        st[1] = C.darts;
+        st[2] = C.hits;
+        st[3] = (uint32_t)phi_star;
+      }
+    }
+    team_sync(G, team);
+  }
+}
+

@@ -280,3 +280,110 @@ def test_host_buffer_abi_matches_device_path():
     assert np.array_equal(bits, as_u64(dev.bits))
     assert np.array_equal(phi, dev.phi.cpu().numpy())
     assert np.array_equal(stats, dev.stats.cpu().numpy().view(np.uint32))
+
+
+# ------------------------------------------------------------------ LSH (K5)
+
+
+def test_lsh_cfg4_golden():
+    g = golden("lsh_cfg4.npz")
+    rows = int(g["rows"])
+    indptr, ids, w = workloads.generate("cfg4", n=rows)
+    assert csr_digest(indptr, ids, w) == str(g["digest"])
+    f = fam(workloads.CONFIGS["cfg4"].seed)
+    res = lsh_batch(indptr, ids, w, LshParams(100, 20), f, fps=True)
+    assert np.array_equal(as_u64(res.keys), g["keys"])
+    assert np.array_equal(as_u64(res.fps)[:4], g["fps"])
+    nres = lsh_batch(indptr, ids, w, LshParams(100, 20), f, normalize=True)
+    assert np.array_equal(as_u64(nres.keys), g["norm_keys"])
+
+
+def test_lsh_small_shapes():
+    g = golden("lsh_small.npz")
+    f = fam(int(g["seed"]))
+    for L, K in ((1, 1), (6, 3), (16, 4), (7, 5)):
+        res = lsh_batch(g["indptr"], g["ids"], g["w"], LshParams(L, K), f, fps=True)
+        assert np.array_equal(as_u64(res.keys), g[f"keys_{L}_{K}"]), (L, K)
+        assert np.array_equal(as_u64(res.fps), g[f"fps_{L}_{K}"]), (L, K)
+
+
+def test_lsh_cfg4_vs_oracle():
+    indptr, ids, w = workloads.generate("cfg4", n=400, start=5000)
+    f = fam(3)
+    res = lsh_batch(indptr, ids, w, LshParams(100, 20), f)
+    keys, _, status, phi, hits = Oracle(3).lsh_csr(indptr, ids, w, 100, 20)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+    assert np.array_equal(res.stats.cpu().numpy().view(np.uint32)[:, 2].astype(np.int64), hits)
+    nres = lsh_batch(indptr, ids, w, LshParams(100, 20), f, normalize=True)
+    nkeys, _, nstatus, _, _ = Oracle(3).lsh_csr(indptr, ids, w, 100, 20, normalize=True)
+    assert np.array_equal(as_u64(nres.keys), nkeys)
+
+
+def test_lsh_key_single_set_api():
+    f = fam(0xA11)
+    x = WeightedSet.from_arrays(np.array([3, 9, 27, 81], dtype=np.uint64),
+                                np.array([0.5, 1.5, 0.25, 2.0]))
+    keys = lsh_key(x, LshParams(6, 3), f)
+    assert len(keys) == 6 and all(len(k) == 3 for k in keys)
+    assert keys == lsh_key(x, LshParams(6, 3), f)
+    # (L, K) = (1, 1) equals the k = 1 minhash (tests/test_annindex.py:75-78)
+    k11 = lsh_key(x, LshParams(1, 1), f)
+    assert k11[0][0] == int(dart_minhash(x, 1, f).values[0])
+    _, fps, _, _, _ = Oracle(0xA11).lsh_csr(np.array([0, 4]), x.ids, x.weights, 6, 3,
+                                             want_fps=True)
+    assert [tuple(int(v) for v in row) for row in fps[0]] == keys
+
+
+def test_darts_random_extreme_weights_vs_oracle():
+    """Weight windows under wide dynamic ranges, many t (exercises rho >= 1
+    regions and the multiplication-based window estimate)."""
+    rng = np.random.default_rng(77)
+    f = fam(0x77)
+    orc = Oracle(0x77)
+    for t in (1, 7, 100, 1000, 5000):
+        sets, limits = [], []
+        for _ in range(40):
+            n = int(rng.integers(1, 30))
+            ids = rng.choice(2**40, size=n, replace=False).astype(np.uint64)
+            w = 2.0 ** rng.uniform(-40, 40, n)
+            l1 = float(np.sum(w))
+            limits.append(float(rng.choice([0.5, 1.0, 2.0, 3.0])) / l1)
+            sets.append((ids, w))
+        indptr = np.zeros(len(sets) + 1, dtype=np.int64)
+        np.cumsum([s[0].size for s in sets], out=indptr[1:])
+        ids = np.concatenate([s[0] for s in sets])
+        w = np.concatenate([s[1] for s in sets])
+        offsets, status, cols = darts_batch(indptr, ids, w, t, np.array(limits), f)
+        st = status.cpu().numpy()
+        off = offsets.cpu().numpy()
+        el = as_u64(cols["element"])
+        fp = as_u64(cols["fingerprint"])
+        rank = cols["rank"].cpu().numpy()
+        for s_i in range(len(sets)):
+            ost, od = orc.darts_below_rank(sets[s_i][0], sets[s_i][1], t, limits[s_i])
+            assert st[s_i] == ost, (t, s_i)
+            if ost:
+                continue
+            a, b = off[s_i], off[s_i + 1]
+            got = sorted(zip(el[a:b].tolist(), fp[a:b].tolist(), rank[a:b].tolist()))
+            exp = sorted(zip(od["element"].tolist(), od["fingerprint"].tolist(),
+                             od["rank"].tolist()))
+            assert got == exp, (t, s_i)
+
+
+def test_lsh_host_buffer_abi():
+    import ctypes
+
+    from paper_2005_11547_b200 import _lib
+    indptr, ids, w = workloads.generate("cfg4", n=500)
+    f = fam(3)
+    dev = lsh_batch(indptr, ids, w, LshParams(100, 20), f)
+    keys = np.zeros((500, 100), dtype=np.uint64)
+    status = np.zeros(500, dtype=np.int32)
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    rc = _lib.load().dsk_lsh_csr_host(f.context(), P(indptr), P(ids), P(w), 500, 100, 20, 0,
+                                     P(keys), None, P(status), None, None)
+    assert rc == 0 and (status == 0).all()
+    assert np.array_equal(keys, as_u64(dev.keys))
