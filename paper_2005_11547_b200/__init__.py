@@ -8,7 +8,7 @@ DESIGN.md for the boundary and INTEGRATION.md for the ctypes binding.
 """
 
 from .constants import ValidationError, minhash_density
-from . import workloads
+from . import shard, workloads
 from .api import (
     DSK_STATUS_TIE,
     Dart,

@@ -387,3 +387,27 @@ def test_lsh_host_buffer_abi():
                                      P(keys), None, P(status), None, None)
     assert rc == 0 and (status == 0).all()
     assert np.array_equal(keys, as_u64(dev.keys))
+
+
+def test_tie_resolution_path():
+    """Rows flagged DSK_STATUS_TIE are re-resolved by full index tuple on the
+    GPU (ref/sketching.py:93-99); force the path on corrupted rows."""
+    from paper_2005_11547_b200 import api
+    indptr, ids, w = workloads.generate("cfg1", n=40)
+    f = fam(0)
+    k = 64
+    res = minhash_batch(indptr, ids, w, k, f, bits=True)
+    good = as_u64(res.values).copy()
+    good_bits = as_u64(res.bits).copy()
+    rows = torch.tensor([3, 17, 29], device=res.values.device)
+    res.values[rows] = 12345
+    res.bits[rows] = 0
+    res.status[rows] = res.status[rows] | DSK_STATUS_TIE
+    dev = res.values.device
+    p = torch.from_numpy(indptr).to(dev)
+    i = torch.from_numpy(ids.view(np.int64)).to(dev)
+    ww = torch.from_numpy(w).to(dev)
+    api._resolve_minhash_ties(res, p, i, ww, k, f, dev)
+    assert np.array_equal(as_u64(res.values), good)
+    assert np.array_equal(as_u64(res.bits), good_bits)
+    assert (res.status.cpu().numpy() == 0).all()

@@ -1,0 +1,78 @@
+"""Multi-process (gloo, world_size 2, CPU) tests of the row-sharding host
+logic: shard planning, local CSR slicing and the optional result gather.
+The GPU compute is stood in for by a row-id function so the test checks that
+every row lands exactly once and in order."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2005_11547_b200 import shard, workloads
+
+
+def test_plan_shards_balanced_and_complete():
+    indptr, _, _ = workloads.generate("cfg5", n=20000)
+    for world in (1, 2, 3, 4, 8):
+        b = shard.plan_shards(indptr, world, t=750)
+        assert b[0] == 0 and b[-1] == 20000 and (np.diff(b) >= 0).all()
+        cost = shard.row_costs(indptr, 750)
+        per = np.array([cost[b[r]:b[r + 1]].sum() for r in range(world)])
+        assert per.max() <= cost.sum() / world + cost.max() + 1e-9
+
+
+def test_shard_csr_slices():
+    indptr, ids, w = workloads.generate("cfg3", n=1000)
+    b = shard.plan_shards(indptr, 3, t=331)
+    got_ids, got_w, rows = [], [], 0
+    for r in range(3):
+        p, i, ww = shard.shard_csr(indptr, ids, w, b, r)
+        assert p[0] == 0 and p[-1] == i.size == ww.size
+        rows += p.size - 1
+        got_ids.append(i)
+        got_w.append(ww)
+    assert rows == 1000
+    assert np.array_equal(np.concatenate(got_ids), ids)
+    assert np.array_equal(np.concatenate(got_w), w)
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    indptr, _, _ = workloads.generate("cfg5", n=3001)
+    bounds = shard.plan_shards(indptr, world, t=750)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    # stand-in for the per-rank GPU result: one row of 4 values per set
+    local = torch.arange(r0, r1, dtype=torch.int64).unsqueeze(1).repeat(1, 4) * 10 + rank
+    full = shard.gather_rows(local, bounds)
+    ok = full.shape == (3001, 4) and bool((full[:, 0] // 10 == torch.arange(3001)).all())
+    owners = (full[:, 0] % 10).numpy()
+    exp = np.concatenate([np.full(int(bounds[r + 1] - bounds[r]), r) for r in range(world)])
+    ok = ok and np.array_equal(owners, exp)
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_gather_rows_gloo(world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=120) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
