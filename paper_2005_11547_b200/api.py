@@ -40,6 +40,8 @@ _STATUS_ERRORS = {
     DSK_AREAS: (ValidationError, "rank limit enumerates too many areas for this density"),
     DSK_NOCONV: (RuntimeError, "bucket filling did not converge; hash family is broken"),
     DSK_LIMIT: (ValidationError, "rank limit must be positive and finite"),
+    7: (RuntimeError, "LSH hit buffer overflow (library limit)"),
+    8: (RuntimeError, "set too large for dart materialisation (>= 4096 elements)"),
 }
 
 

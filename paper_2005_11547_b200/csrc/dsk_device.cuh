@@ -88,12 +88,18 @@ __device__ __forceinline__ int64_t weight_window(double x, double w0, double dnu
   double base = floor(__dmul_rn(__dadd_rn(x, -w0), tpow));
   base = base < capw ? base : capw;  // np.minimum
   base = base > 0.0 ? base : 0.0;    // np.maximum
-#pragma unroll
-  for (int delta = 2; delta >= -2; --delta) {
-    double cand = base + (double)delta;
-    if (cand >= 0.0 && cand <= wmax && __dadd_rn(w0, __dmul_rn(cand, dnu)) <= x)
-      return (int64_t)cand;
+  // The reference takes the first passing candidate of base+2, ..., base-2;
+  // the predicate is monotone in c, so that is the largest passing one --
+  // found here from base outwards (usually two evaluations instead of three).
+  auto pass = [&](double cand) {
+    return cand >= 0.0 && cand <= wmax && __dadd_rn(w0, __dmul_rn(cand, dnu)) <= x;
+  };
+  if (pass(base)) {
+    if (!pass(base + 1.0)) return (int64_t)base;
+    return pass(base + 2.0) ? (int64_t)(base + 2.0) : (int64_t)(base + 1.0);
   }
+  if (pass(base - 1.0)) return (int64_t)(base - 1.0);
+  if (pass(base - 2.0)) return (int64_t)(base - 2.0);
   return -1;
 }
 

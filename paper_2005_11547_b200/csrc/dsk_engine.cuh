@@ -2,13 +2,23 @@
 //
 // Restates DartHasher.dart_batch (ref/darthash.py:142-295) for the GPU.  One
 // warp walks the elements of its share of a set and expands work through four
-// load-balanced levels, each backed by a 64-entry shared-memory queue so every
-// stage runs on full 32-lane batches:
+// load-balanced levels, each backed by a shared-memory ring so every stage
+// runs on full batches:
 //
-//   element chunk --(depth+1)(rank_depth+1)--> regions (nu, rho)   [region queue]
-//   region  --(w_hi+1)(r_hi-r_lo+1)--> areas (w, r) + Poisson count [area queue]
-//   area    --count--> candidate darts, rank/weight filter       -> [hit queue]
+//   element chunk --(depth+1)(rank_depth+1)--> regions (nu, rho)   [region ring]
+//   region  --(w_hi+1)(r_hi-r_lo+1)--> areas (w, r) + Poisson count [area ring]
+//   area    --count--> candidate darts, rank/weight filter       -> [hit ring]
 //   hit     --> fingerprint, bucket hash, Sink (slot minimum / LSH buffer)
+//
+// Scheduling is a flat, warp-uniform "pull" loop: each iteration runs the
+// deepest stage that has a full batch ready (hits >= 64, areas >= 32,
+// regions >= 32, else the next 64 regions of the element chunk).  A stage
+// consumes at most 64 children of the parents at the head of its ring,
+// keeping a child cursor, and produces at most 64 items downstream; with
+// downstream-first priority every ring stays below its capacity.  Each stage
+// body exists once in the code (small I-cache footprint) and evaluates two
+// independent children per lane (positions lo+lane and lo+32+lane) in
+// straight-line code, so their dependent hash / fp64 chains interleave.
 //
 // Hashing is tabulation + splitmix64 (ref/randomness.py:121-131) with the
 // constant key bytes hoisted: the element's 8-byte XOR once per element, nu
@@ -21,18 +31,18 @@
 // the next row's corner) and are skipped; the shared row r_lo is filtered on
 // the computed rank.  The union of the bands 1..phi equals the reference's
 // from-scratch recompute at phi (prefix property).
-//
-// Queue records are 16-byte words in structure-of-arrays layout so each
-// field group moves with one conflict-free LDS.128 / STS.128.
 #pragma once
 #include "dsk_device.cuh"
 
 namespace dsk {
 
-constexpr int kWarps = 24;   // warps per CTA (one CTA per SM)
-constexpr int kQ = 64;       // queue capacity per level
+constexpr int kILP = 1;      // children per lane per stage step (independent chains)
+constexpr int kStep = 32 * kILP;
+constexpr int kWarps = kILP == 1 ? 24 : 12;  // warps per CTA (one CTA per SM)
+constexpr int kQR = 64 * kILP;  // region / area ring capacity (>= 31 + kStep); power of two
+constexpr int kQ = 64 * kILP;   // hit ring capacity (>= kStep - 1 + kStep); power of two
 constexpr int kJs = 64;      // folded (j, stream) table rows; Poisson counts < 64
-constexpr int kRwin = 128;   // per-pass rank-window table entries per warp
+constexpr int kRwin = 128;   // per-pass rank-window table entries
 
 struct SmemTables {
   uint64_t tE[8][256];    // T0..T7  element bytes
@@ -51,17 +61,18 @@ struct SmemTables {
 };
 
 struct WarpQueues {
-  ulonglong2 rgA[kQ];   // region: {P_R, x}
-  uint4 rgB[kQ];        //         {w_hi, r_lo, r_hi, meta}
-  ulonglong2 arA[kQ];   // area:   {P_A, x}
-  uint4 arB[kQ];        //         {w, r, meta, element index (materialising sink)}
+  ulonglong2 rgA[kQR];  // region: {P_R, x}
+  uint4 rgB[kQR];       //         {w_hi, r_lo, r_hi, meta}
+  ulonglong2 arA[kQR];  // area:   {P_A, x}
+  uint4 arB[kQR];       //         {w, r, meta, element index (materialising sink)}
   ulonglong2 ht[kQ];    // hit:    {P_A ^ js[j][fp], rank bits}
   ulonglong2 el[32];    // element chunk: {E, x}
   uint32_t elIdx[32];
 };
 
-// region meta: nu | rho << 8 | flags << 16 (| element index << 19, materialising sink)
-constexpr uint32_t kRgHasPrev = 1u << 16, kRgWide = 1u << 17, kRgNarrow = 1u << 18;
+// region meta: nu | rho << 8 | flags << 16 (| element index << 20, materialising sink)
+constexpr uint32_t kRgHasPrev = 1u << 16, kRgWide = 1u << 17, kRgNarrow = 1u << 18,
+                   kRgWEdge = 1u << 19;  // the w_hi column can hold darts heavier than x
 // area meta: nu | rho << 8 | count << 16 | flags << 24
 constexpr uint32_t kArWb = 1u << 24, kArRb = 1u << 25, kArLb = 1u << 26;
 
@@ -102,6 +113,48 @@ __device__ __forceinline__ uint32_t poisson_count(uint64_t X, const PassParams &
   return c;
 }
 
+// Parents at the head of a ring, expanded into children in steps of <= 64:
+// scan of the first <= 32 parents' child counts.
+struct HeadScan {
+  uint32_t excl, incl, total;
+  int mp;
+};
+
+__device__ __forceinline__ HeadScan head_scan(uint32_t c, int mp, int lane) {
+  HeadScan h;
+  h.mp = mp;
+  h.incl = warp_incl_scan(c, lane);
+  h.total = __shfl_sync(DSK_FULL, h.incl, 31);
+  h.excl = h.incl - c;
+  return h;
+}
+
+// After consuming children [cursor, hi) of the head parents: how many parents
+// are exhausted, and the cursor into the first remaining one.
+__device__ __forceinline__ void head_pop(const HeadScan &h, uint32_t hi, int lane, int &npop,
+                                         uint32_t &cursor) {
+  unsigned done = __ballot_sync(DSK_FULL, lane < h.mp && h.incl <= hi);
+  npop = __popc(done);
+  uint32_t consumed = __shfl_sync(DSK_FULL, h.incl, npop > 0 ? npop - 1 : 0);
+  cursor = hi - (npop > 0 ? consumed : 0);
+}
+
+__device__ __forceinline__ int ringR(uint32_t x) { return (int)(x & (uint32_t)(kQR - 1)); }
+
+// rank windows of one (nu, rho) for the rare sets whose (depth, rank depth)
+// grid exceeds the per-pass table (kept out of line: cold code)
+__device__ __noinline__ void rank_windows_slow(const PassParams &P, int nu, int rho,
+                                               int64_t &r_hi, int64_t &r_lo, uint32_t &flags) {
+  double r0 = __dadd_rn(pow2(rho), -1.0);
+  double drho = pow2(rho - nu);
+  r_hi = rank_window(P.L_hi, nu, rho, r0, drho);
+  r_lo = 0;
+  if (P.L_lo >= 0.0 && rho <= P.RD_lo) {
+    int64_t rp = rank_window(P.L_lo, nu, rho, r0, drho);
+    if (rp >= 0) { r_lo = rp; flags |= kRgHasPrev >> 16; }
+  }
+}
+
 template <class Sink, bool kFull>
 struct Engine {
   const SmemTables &T;
@@ -111,11 +164,14 @@ struct Engine {
   const PassParams P;
   int lane;
   int rg_head = 0, rg_cnt = 0, ar_head = 0, ar_cnt = 0, ht_head = 0, ht_cnt = 0;
+  uint32_t rg_cur = 0, ar_cur = 0;
   bool use_table = false;
   bool abort = false;       // warp-uniform: area cap exceeded by one lane's share
   double lane_full = 0.0;   // per lane: areas of the full (non-band) step (area cap)
   uint32_t n_darts = 0;     // per lane: candidate darts first seen in this band
   uint32_t n_hits = 0;      // per lane
+  // element chunk state: lane i holds element i's region-count scan
+  uint32_t el_excl = 0, el_total = 0, el_cur = 0;
 
   __device__ Engine(const SmemTables &t, WarpQueues &q, uint2 *rw, Sink &s, const PassParams &p,
                     int ln)
@@ -144,213 +200,233 @@ struct Engine {
     __syncwarp();
   }
 
-  // ---------------------------------------------------------------- hits
-  __device__ void process_hits(int m) {
-    int idx = (ht_head + lane) & (kQ - 1);
-    bool valid = lane < m;
-    HitInfo h;
-    h.rank = 0.0; h.fp = 0; h.bhash = 0;
-    if (valid) {
-      ulonglong2 rec = Q.ht[idx];
-      h.rank = __longlong_as_double((long long)rec.y);
-      h.fp = finalize(rec.x);  // fingerprint, ref/randomness.py:149-152
-      uint64_t f = h.fp;
-      uint64_t x = T.bconst;   // hash64(fp, stream=5), ref/randomness.py:154-158
-#pragma unroll
-      for (int p = 0; p < 8; p++) x ^= T.tE[p][(f >> (8 * p)) & 0xff];
-      h.bhash = finalize(x);
-      n_hits++;
-    }
-    ht_head = (ht_head + m) & (kQ - 1);
-    ht_cnt -= m;
-    sink.hit(valid, h, lane);
-  }
-
-  __device__ void drain_hits(bool force) {
-    while (ht_cnt >= 32 || (force && ht_cnt > 0)) process_hits(ht_cnt < 32 ? ht_cnt : 32);
-  }
-
-  __device__ void push_hit(bool valid, double rank, uint64_t fpkey) {
+  // ---------------------------------------------------------------- pushes
+  // (no draining here: the scheduler keeps every ring below capacity)
+  __device__ __forceinline__ void push_hit(bool valid, double rank, uint64_t fpkey) {
     unsigned b = __ballot_sync(DSK_FULL, valid);
-    if (b == 0) return;
     if (valid) {
       int idx = (ht_head + ht_cnt + __popc(b & ((1u << lane) - 1))) & (kQ - 1);
       Q.ht[idx] = make_ulonglong2(fpkey, (unsigned long long)__double_as_longlong(rank));
     }
     ht_cnt += __popc(b);
-    __syncwarp();
-    if (ht_cnt >= 32) drain_hits(false);
   }
 
-  // --------------------------------------------------------------- darts
-  // Expand up to 32 queued areas into their Poisson(1) darts
-  // (ref/darthash.py:264-292).
-  __device__ void process_areas(int m) {
-    int head = ar_head;
-    ar_head = (ar_head + m) & (kQ - 1);
-    ar_cnt -= m;
-    uint32_t c = 0;
-    if (lane < m) c = (Q.arB[(head + lane) & (kQ - 1)].z >> 16) & 0xff;
-    uint32_t incl = warp_incl_scan(c, lane);
-    uint32_t total = __shfl_sync(DSK_FULL, incl, 31);
-    uint32_t excl = incl - c;
-    for (uint32_t base = 0; base < total; base += 32) {
-      uint32_t pos = base + lane;
-      bool valid = pos < total;
-      int src = warp_owner(excl, pos);
-      uint32_t j = pos - __shfl_sync(DSK_FULL, excl, src);
-      bool hit = false;
-      double rank = 0.0, weight = 0.0;
-      uint64_t pa = 0;
-      uint4 B = make_uint4(0, 0, 0, 0);
-      if (valid) {
-        int ai = (head + src) & (kQ - 1);
-        ulonglong2 A = Q.arA[ai];
-        B = Q.arB[ai];
-        pa = A.x;
-        uint32_t meta = B.z;
-        int nu = meta & 0xff, rho = (meta >> 8) & 0xff;
-        // rank = r0 + (r + u) * drho, ref/darthash.py:282 (separately rounded)
-        double u = u53(finalize(pa ^ T.js[j][kStreamU - 1]));
-        double r0 = __dadd_rn(pow2(rho), -1.0);
-        rank = __dadd_rn(r0, __dmul_rn(__dadd_rn((double)B.y, u), pow2(rho - nu)));
-        hit = true;
-        if (meta & kArRb) hit = rank <= P.L_hi;        // interior rows pass by monotonicity
-        if (meta & kArLb) hit = hit && rank > P.L_lo;  // band: exclude darts seen before
-        if (kFull || (hit && (meta & kArWb))) {        // only the w_hi column can miss
-          double v = u53(finalize(pa ^ T.js[j][kStreamV - 1]));
-          double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
-          // weight = w0 + (w + v) * dnu, ref/darthash.py:281
-          weight = __dadd_rn(T.w0[nu], __dmul_rn(__dadd_rn((double)B.x, v), dnu));
-          double x = __longlong_as_double((long long)A.y);
-          if (meta & kArWb) hit = hit && weight <= x;  // ref/darthash.py:284 (inclusive)
-        }
-      }
-      if (kFull) {  // materialising sink: every hit with its full index tuple
-        if (hit) {
-          DartRow d;
-          d.elem = B.w;
-          d.nu = B.z & 0xff;
-          d.rho = (B.z >> 8) & 0xff;
-          d.w = B.x;
-          d.r = B.y;
-          d.j = j;
-          d.weight = weight;
-          d.rank = rank;
-          d.fp = finalize(pa ^ T.js[j][kStreamFp - 1]);
-          sink.row(d);
-          n_hits++;
-        }
-      } else {
-        push_hit(hit, rank, pa ^ T.js[j][kStreamFp - 1]);
-      }
-    }
-  }
-
-  __device__ void drain_areas(bool force) {
-    while (ar_cnt >= 32 || (force && ar_cnt > 0)) process_areas(ar_cnt < 32 ? ar_cnt : 32);
-  }
-
-  __device__ void push_area(bool valid, uint64_t pa, double x, uint32_t w, uint32_t r,
-                            uint32_t meta, uint32_t elem) {
+  __device__ __forceinline__ void push_area(bool valid, uint64_t pa, double x, uint32_t w,
+                                            uint32_t r, uint32_t meta, uint32_t elem) {
     unsigned b = __ballot_sync(DSK_FULL, valid);
-    if (b == 0) return;
     if (valid) {
-      int idx = (ar_head + ar_cnt + __popc(b & ((1u << lane) - 1))) & (kQ - 1);
+      int idx = ringR(ar_head + ar_cnt + __popc(b & ((1u << lane) - 1)));
       Q.arA[idx] = make_ulonglong2(pa, (unsigned long long)__double_as_longlong(x));
       Q.arB[idx] = make_uint4(w, r, meta, elem);
     }
     ar_cnt += __popc(b);
-    __syncwarp();
-    if (ar_cnt >= 32) drain_areas(false);
   }
 
-  // --------------------------------------------------------------- areas
-  // Expand up to 32 queued regions into their (w, r) areas, w-major
-  // (ref/darthash.py:248-262), with the Poisson(1) count of each.
-  __device__ void process_regions(int m) {
-    int head = rg_head;
-    rg_head = (rg_head + m) & (kQ - 1);
-    rg_cnt -= m;
-    uint32_t c = 0;
-    if (lane < m) {
-      uint4 B = Q.rgB[(head + lane) & (kQ - 1)];
-      c = (B.x + 1) * (B.z - B.y + 1);
-    }
-    uint32_t incl = warp_incl_scan(c, lane);
-    uint32_t total = __shfl_sync(DSK_FULL, incl, 31);
-    uint32_t excl = incl - c;
-    for (uint32_t base = 0; base < total; base += 32) {
-      uint32_t pos = base + lane;
-      bool valid = pos < total;
-      int src = warp_owner(excl, pos);
-      uint32_t off = pos - __shfl_sync(DSK_FULL, excl, src);
-      bool keep = false;
-      uint64_t pa = 0;
-      double x = 0.0;
-      uint32_t w = 0, r = 0, meta = 0, elem = 0;
-      if (valid) {
-        int gi = (head + src) & (kQ - 1);
-        ulonglong2 A = Q.rgA[gi];
-        uint4 B = Q.rgB[gi];
-        uint32_t whi = B.x, rlo = B.y, rhi = B.z, rmeta = B.w;
-        if (whi == 0) {
-          w = 0;
-          r = rlo + off;
-        } else {
-          uint32_t rc = rhi - rlo + 1;
-          w = off / rc;
-          r = rlo + (off - w * rc);
-        }
-        pa = A.x;
-        if (rmeta & kRgNarrow) {
-          pa ^= T.tW[0][w] ^ T.tR[0][r];
-        } else {
-          pa ^= T.tW[0][w & 0xff] ^ T.tW[1][(w >> 8) & 0xff] ^ T.tR[0][r & 0xff] ^
-                T.tR[1][(r >> 8) & 0xff];
-          if (rmeta & kRgWide)
-            pa ^= __ldg(&P.gtab[12 * 256 + ((w >> 16) & 0xff)]) ^
-                  __ldg(&P.gtab[13 * 256 + (w >> 24)]) ^
-                  __ldg(&P.gtab[16 * 256 + ((r >> 16) & 0xff)]) ^
-                  __ldg(&P.gtab[17 * 256 + (r >> 24)]);
-        }
-        // poisson1, ref/randomness.py:145-147 / :209-211 (j = 0, stream 3)
-        uint32_t cnt = poisson_count(finalize(pa ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
-        bool lb = (rmeta & kRgHasPrev) && r == rlo;
-        if (!lb) n_darts += cnt;
-        keep = cnt > 0;
-        meta = (rmeta & 0xffff) | (cnt << 16) | (w == whi ? kArWb : 0) | (r == rhi ? kArRb : 0) |
-               (lb ? kArLb : 0);
-        x = __longlong_as_double((long long)A.y);
-        if (kFull) elem = rmeta >> 19;  // materialising sink: element index
-      }
-      push_area(keep, pa, x, w, r, meta, elem);
-    }
-  }
-
-  __device__ void drain_regions(bool force) {
-    while (rg_cnt >= 32 || (force && rg_cnt > 0)) process_regions(rg_cnt < 32 ? rg_cnt : 32);
-  }
-
-  __device__ void push_region(bool valid, uint64_t pr, double x, uint32_t whi, uint32_t rlo,
-                              uint32_t rhi, uint32_t meta) {
+  __device__ __forceinline__ void push_region(bool valid, uint64_t pr, double x, uint32_t whi,
+                                              uint32_t rlo, uint32_t rhi, uint32_t meta) {
     unsigned b = __ballot_sync(DSK_FULL, valid);
-    if (b == 0) return;
     if (valid) {
-      int idx = (rg_head + rg_cnt + __popc(b & ((1u << lane) - 1))) & (kQ - 1);
+      int idx = ringR(rg_head + rg_cnt + __popc(b & ((1u << lane) - 1)));
       Q.rgA[idx] = make_ulonglong2(pr, (unsigned long long)__double_as_longlong(x));
       Q.rgB[idx] = make_uint4(whi, rlo, rhi, meta);
     }
     rg_cnt += __popc(b);
-    __syncwarp();
-    if (rg_cnt >= 32) drain_regions(false);
   }
 
-  // ------------------------------------------------------------- regions
-  // One element chunk (<= 32 elements, lane i holds element i): expand each
-  // element into its (nu, rho) regions and compute the surviving rectangle
-  // (ref/darthash.py:180-225).  Sets `abort` when the area cap trips.
-  __device__ void element_chunk(bool valid, uint64_t id, double x, int depth, uint32_t eidx) {
+  // ----------------------------------------------------------------- hits
+  __device__ __forceinline__ void hit_keys(int idx, HitInfo &h) {
+    ulonglong2 rec = Q.ht[idx];
+    h.rank = __longlong_as_double((long long)rec.y);
+    h.fp = finalize(rec.x);  // fingerprint, ref/randomness.py:149-152
+    uint64_t x = T.bconst;   // hash64(fp, stream=5), ref/randomness.py:154-158
+#pragma unroll
+    for (int p = 0; p < 8; p++) x ^= T.tE[p][(h.fp >> (8 * p)) & 0xff];
+    h.bhash = finalize(x);
+  }
+
+  __device__ void hits_step() {
+    const int m = ht_cnt < kStep ? ht_cnt : kStep;
+    HitInfo h[kILP];
+#pragma unroll
+    for (int q = 0; q < kILP; q++) hit_keys((ht_head + 32 * q + lane) & (kQ - 1), h[q]);
+#pragma unroll
+    for (int q = 0; q < kILP; q++) n_hits += (uint32_t)(lane + 32 * q < m);
+    ht_head = (ht_head + m) & (kQ - 1);
+    ht_cnt -= m;
+#pragma unroll
+    for (int q = 0; q < kILP; q++)
+      if (m > 32 * q) sink.hit(lane + 32 * q < m, h[q], lane);
+  }
+
+  // ---------------------------------------------------------------- darts
+  // darts [ar_cur, ar_cur + 64) of the head areas (ref/darthash.py:264-292)
+  __device__ void areas_step() {
+    const int mp = ar_cnt < 32 ? ar_cnt : 32;
+    uint32_t c = lane < mp ? (Q.arB[ringR(ar_head + lane)].z >> 16) & 0xff : 0;
+    HeadScan hs = head_scan(c, mp, lane);
+    const uint32_t lo = ar_cur, hi = lo + kStep < hs.total ? lo + kStep : hs.total;
+    bool valid[kILP], hit[kILP], needv[kILP];
+    uint32_t j[kILP], meta[kILP];
+    int ai[kILP];
+    uint64_t pa[kILP];
+    double rank[kILP], x[kILP];
+    uint4 B[kILP];
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      uint32_t pos = lo + lane + 32 * q;
+      valid[q] = pos < hi;
+      int src = warp_owner(hs.excl, pos);
+      j[q] = (pos - __shfl_sync(DSK_FULL, hs.excl, src)) & (kJs - 1);
+      ai[q] = ringR(ar_head + src);
+    }
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      ulonglong2 A = Q.arA[ai[q]];
+      B[q] = Q.arB[ai[q]];
+      pa[q] = A.x;
+      x[q] = __longlong_as_double((long long)A.y);
+      meta[q] = B[q].z;
+    }
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      // rank = r0 + (r + u) * drho, ref/darthash.py:282 (separately rounded)
+      int nu = meta[q] & 0xff, rho = (meta[q] >> 8) & 0xff;
+      double u = u53(finalize(pa[q] ^ T.js[j[q]][kStreamU - 1]));
+      double r0 = __dadd_rn(pow2(rho), -1.0);
+      rank[q] = __dadd_rn(r0, __dmul_rn(__dadd_rn((double)B[q].y, u), pow2(rho - nu)));
+      bool h = valid[q];
+      if (meta[q] & kArRb) h = h && rank[q] <= P.L_hi;  // interior rows pass by monotonicity
+      if (meta[q] & kArLb) h = h && rank[q] > P.L_lo;   // band: exclude darts seen before
+      needv[q] = h && (kFull || (meta[q] & kArWb));     // only the w_hi column can miss
+      hit[q] = h;
+    }
+    double weight[kILP];
+    bool anyv = false;
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      weight[q] = 0.0;
+      anyv = anyv || needv[q];
+    }
+    if (__any_sync(DSK_FULL, anyv)) {
+#pragma unroll
+      for (int q = 0; q < kILP; q++) {
+        int nu = meta[q] & 0xff, rho = (meta[q] >> 8) & 0xff;
+        double v = u53(finalize(pa[q] ^ T.js[j[q]][kStreamV - 1]));
+        double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
+        // weight = w0 + (w + v) * dnu, ref/darthash.py:281
+        weight[q] = __dadd_rn(T.w0[nu], __dmul_rn(__dadd_rn((double)B[q].x, v), dnu));
+        if (needv[q] && (meta[q] & kArWb)) hit[q] = weight[q] <= x[q];  // inclusive, :284
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      if (kFull) {  // materialising sink: every hit with its full index tuple
+        if (hit[q]) {
+          DartRow d;
+          d.elem = B[q].w;
+          d.nu = meta[q] & 0xff;
+          d.rho = (meta[q] >> 8) & 0xff;
+          d.w = B[q].x;
+          d.r = B[q].y;
+          d.j = j[q];
+          d.weight = weight[q];
+          d.rank = rank[q];
+          d.fp = finalize(pa[q] ^ T.js[j[q]][kStreamFp - 1]);
+          sink.row(d);
+          n_hits++;
+        }
+      } else {
+        push_hit(hit[q], rank[q], pa[q] ^ T.js[j[q]][kStreamFp - 1]);
+      }
+    }
+    int npop;
+    head_pop(hs, hi, lane, npop, ar_cur);
+    ar_head = ringR(ar_head + npop);
+    ar_cnt -= npop;
+    __syncwarp();
+  }
+
+  // ---------------------------------------------------------------- areas
+  // areas [rg_cur, rg_cur + 64) of the head regions, w-major
+  // (ref/darthash.py:248-262), with the Poisson(1) count of each
+  // (ref/randomness.py:145-147, :209-211: j = 0, stream 3)
+  __device__ void regions_step() {
+    const int mp = rg_cnt < 32 ? rg_cnt : 32;
+    uint32_t c = 0;
+    if (lane < mp) {
+      uint4 b = Q.rgB[ringR(rg_head + lane)];
+      c = (b.x + 1) * (b.z - b.y + 1);
+    }
+    HeadScan hs = head_scan(c, mp, lane);
+    const uint32_t lo = rg_cur, hi = lo + kStep < hs.total ? lo + kStep : hs.total;
+    bool valid[kILP];
+    uint32_t w[kILP], r[kILP], rmeta[kILP], rlo[kILP], whi[kILP], rhi[kILP];
+    uint64_t pa[kILP];
+    double x[kILP];
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      uint32_t pos = lo + lane + 32 * q;
+      valid[q] = pos < hi;
+      int src = warp_owner(hs.excl, pos);
+      uint32_t base = __shfl_sync(DSK_FULL, hs.excl, src);
+      uint32_t off = valid[q] ? pos - base : 0;
+      int gi = ringR(rg_head + src);
+      ulonglong2 A = Q.rgA[gi];
+      uint4 B = Q.rgB[gi];
+      whi[q] = B.x; rlo[q] = B.y; rhi[q] = B.z; rmeta[q] = B.w;
+      pa[q] = A.x;
+      x[q] = __longlong_as_double((long long)A.y);
+      uint32_t rc = rhi[q] - rlo[q] + 1;
+      uint32_t ww;
+      if (whi[q] == 0 || !valid[q]) {
+        ww = 0;
+      } else if (off < (1u << 20)) {  // fp32 quotient, off by at most one: corrected
+        ww = (uint32_t)(((float)off + 0.5f) * __frcp_rn((float)rc));
+        if (ww * rc > off) ww--;
+        else if ((ww + 1) * rc <= off) ww++;
+      } else {
+        ww = off / rc;
+      }
+      w[q] = ww;
+      r[q] = rlo[q] + (off - ww * rc);
+    }
+    uint32_t cnt[kILP];
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      uint64_t p = pa[q];
+      if (rmeta[q] & kRgNarrow) {
+        p ^= T.tW[0][w[q] & 0xff] ^ T.tR[0][r[q] & 0xff];
+      } else {
+        p ^= T.tW[0][w[q] & 0xff] ^ T.tW[1][(w[q] >> 8) & 0xff] ^ T.tR[0][r[q] & 0xff] ^
+             T.tR[1][(r[q] >> 8) & 0xff];
+        if (rmeta[q] & kRgWide)
+          p ^= __ldg(&P.gtab[12 * 256 + ((w[q] >> 16) & 0xff)]) ^
+               __ldg(&P.gtab[13 * 256 + (w[q] >> 24)]) ^
+               __ldg(&P.gtab[16 * 256 + ((r[q] >> 16) & 0xff)]) ^
+               __ldg(&P.gtab[17 * 256 + (r[q] >> 24)]);
+      }
+      pa[q] = p;
+      uint32_t k = poisson_count(finalize(p ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
+      cnt[q] = valid[q] ? k : 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      bool lb = (rmeta[q] & kRgHasPrev) && r[q] == rlo[q];
+      if (!lb) n_darts += cnt[q];
+      uint32_t meta = (rmeta[q] & 0xffff) | (cnt[q] << 16) |
+                      (w[q] == whi[q] && (rmeta[q] & kRgWEdge) ? kArWb : 0) |
+                      (r[q] == rhi[q] ? kArRb : 0) | (lb ? kArLb : 0);
+      push_area(cnt[q] > 0, pa[q], x[q], w[q], r[q], meta, kFull ? rmeta[q] >> 20 : 0);
+    }
+    int npop;
+    head_pop(hs, hi, lane, npop, rg_cur);
+    rg_head = ringR(rg_head + npop);
+    rg_cnt -= npop;
+    __syncwarp();
+  }
+
+  // -------------------------------------------------------------- regions
+  __device__ void load_chunk(bool valid, uint64_t id, double x, int depth, uint32_t eidx) {
     uint64_t E = 0;
     if (valid) {
 #pragma unroll
@@ -360,33 +436,46 @@ struct Engine {
     Q.el[lane] = make_ulonglong2(E, (unsigned long long)__double_as_longlong(x));
     if (kFull) Q.elIdx[lane] = eidx;
     __syncwarp();
+    uint32_t c = valid ? (uint32_t)(depth + 1) * (uint32_t)(P.RD + 1) : 0;
+    uint32_t incl = warp_incl_scan(c, lane);
+    el_total = __shfl_sync(DSK_FULL, incl, 31);
+    el_excl = incl - c;
+    el_cur = 0;
+  }
+
+  // regions [el_cur, el_cur + 64) of the element chunk: the surviving
+  // rectangle of each (nu, rho) (ref/darthash.py:180-225)
+  __device__ void element_step() {
     const int rdp1 = P.RD + 1;
     const float inv_rdp1 = 1.0f / (float)rdp1;
-    uint32_t c = valid ? (uint32_t)(depth + 1) * (uint32_t)rdp1 : 0;
-    uint32_t incl = warp_incl_scan(c, lane);
-    uint32_t total = __shfl_sync(DSK_FULL, incl, 31);
-    uint32_t excl = incl - c;
-    for (uint32_t base = 0; base < total; base += 32) {
-      uint32_t pos = base + lane;
-      bool ok = pos < total;
-      int src = warp_owner(excl, pos);
-      uint32_t idx = pos - __shfl_sync(DSK_FULL, excl, src);
-      uint64_t pr = 0;
-      double xs = 0.0;
-      uint32_t whi = 0, rlo = 0, rhi = 0, meta = 0;
-      if (ok) {
-        int nu, rho;
-        if (rdp1 == 1) {
-          nu = (int)idx;
-          rho = 0;
-        } else {  // fp32 quotient, off by at most one: corrected below
-          nu = (int)(((float)idx + 0.5f) * inv_rdp1);
-          rho = (int)idx - nu * rdp1;
-          if (rho < 0) { nu--; rho += rdp1; }
-          else if (rho >= rdp1) { nu++; rho -= rdp1; }
-        }
-        ulonglong2 el = Q.el[src];
-        xs = __longlong_as_double((long long)el.y);
+    const uint32_t lo = el_cur, hi = lo + kStep < el_total ? lo + kStep : el_total;
+    bool ok[kILP];
+    uint64_t pr[kILP];
+    double xs[kILP];
+    uint32_t owhi[kILP], orlo[kILP], orhi[kILP], ometa[kILP];
+#pragma unroll
+    for (int q = 0; q < kILP; q++) {
+      uint32_t pos = lo + lane + 32 * q;
+      const bool valid = pos < hi;
+      int src = warp_owner(el_excl, pos);
+      uint32_t idx = pos - __shfl_sync(DSK_FULL, el_excl, src);
+      int nu, rho;
+      if (rdp1 == 1) {
+        nu = (int)idx;
+        rho = 0;
+      } else {  // fp32 quotient, off by at most one: corrected below
+        nu = (int)(((float)idx + 0.5f) * inv_rdp1);
+        rho = (int)idx - nu * rdp1;
+        if (rho < 0) { nu--; rho += rdp1; }
+        else if (rho >= rdp1) { nu++; rho -= rdp1; }
+      }
+      nu &= 255;
+      rho &= 255;
+      ulonglong2 el = Q.el[src];
+      xs[q] = __longlong_as_double((long long)el.y);
+      ok[q] = false;
+      pr[q] = 0; owhi[q] = 0; orlo[q] = 0; orhi[q] = 0; ometa[q] = 0;
+      if (valid) {
         int64_t r_hi, r_lo = 0;
         uint32_t flags = 0;
         if (use_table) {
@@ -394,48 +483,87 @@ struct Engine {
           r_hi = (int64_t)rw.x - 1;
           if (rw.y & 0x80000000u) { r_lo = rw.y & 0x7fffffffu; flags |= kRgHasPrev >> 16; }
         } else {
-          double r0 = __dadd_rn(pow2(rho), -1.0);
-          double drho = pow2(rho - nu);
-          r_hi = rank_window(P.L_hi, nu, rho, r0, drho);
-          if (P.L_lo >= 0.0 && rho <= P.RD_lo) {
-            int64_t rp = rank_window(P.L_lo, nu, rho, r0, drho);
-            if (rp >= 0) { r_lo = rp; flags |= kRgHasPrev >> 16; }
-          }
+          rank_windows_slow(P, nu, rho, r_hi, r_lo, flags);
         }
         int64_t w_hi = -1;
+        bool wedge = true;
         if (r_hi >= 0) {
           double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
-          w_hi = weight_window(xs, T.w0[nu], dnu, __dmul_rn(P.tf, pow2(rho - nu)), rho);
+          w_hi = weight_window(xs[q], T.w0[nu], dnu, __dmul_rn(P.tf, pow2(rho - nu)), rho);
+          // every dart of column w_hi weighs <= fl(w0 + fl((w_hi+1)*dnu)) by monotone
+          // rounding; when that edge is <= x no dart of the region can miss
+          wedge = __dadd_rn(T.w0[nu], __dmul_rn((double)(w_hi + 1), dnu)) > xs[q];
         }
-        ok = w_hi >= 0 && r_lo <= r_hi;
+        bool okq = w_hi >= 0 && r_lo <= r_hi;
         if (w_hi >= 0) {
           double full = (double)(w_hi + 1) * (double)(r_hi + 1);
           lane_full += full;
           // a region over the cap makes the step illegal (ref/darthash.py:242-244)
-          if (full > kMaxAreas) ok = false;
+          if (full > kMaxAreas) okq = false;
         }
-        if (ok) {
-          whi = (uint32_t)w_hi; rlo = (uint32_t)r_lo; rhi = (uint32_t)r_hi;
-          pr = el.x ^ T.tNu[nu] ^ T.tRho[rho];
+        if (okq) {
+          owhi[q] = (uint32_t)w_hi; orlo[q] = (uint32_t)r_lo; orhi[q] = (uint32_t)r_hi;
+          uint64_t p = el.x ^ T.tNu[nu] ^ T.tRho[rho];
           if (w_hi >= 65536 || r_hi >= 65536) flags |= kRgWide >> 16;
-          else pr ^= T.cfold;
-          if (w_hi < 256 && r_hi < 256) { flags |= kRgNarrow >> 16; pr ^= T.nfold; }
-          meta = (uint32_t)nu | ((uint32_t)rho << 8) | (flags << 16);
-          if (kFull) meta |= Q.elIdx[src] << 19;
+          else p ^= T.cfold;
+          if (w_hi < 256 && r_hi < 256) { flags |= kRgNarrow >> 16; p ^= T.nfold; }
+          if (wedge) flags |= kRgWEdge >> 16;
+          pr[q] = p;
+          ometa[q] = (uint32_t)nu | ((uint32_t)rho << 8) | (flags << 16);
+          if (kFull) ometa[q] |= Q.elIdx[src] << 20;
         }
+        ok[q] = okq;
       }
-      // Any lane whose share exceeds the cap proves the step illegal; the exact
-      // team-wide sum is checked after the pass.  Every queued region then
-      // holds <= 2^27 areas.
-      if (__any_sync(DSK_FULL, lane_full > kMaxAreas)) { abort = true; return; }
-      push_region(ok, pr, xs, whi, rlo, rhi, meta);
     }
+    // Any lane whose share exceeds the cap proves the step illegal; the exact
+    // team-wide sum is checked after the pass.  Every queued region then
+    // holds <= 2^27 areas.
+    if (__any_sync(DSK_FULL, lane_full > kMaxAreas)) {
+      abort = true;
+      return;
+    }
+#pragma unroll
+    for (int q = 0; q < kILP; q++)
+      push_region(ok[q], pr[q], xs[q], owhi[q], orlo[q], orhi[q], ometa[q]);
+    el_cur = hi;
+    __syncwarp();
   }
 
-  __device__ void finish() {
-    drain_regions(true);
-    drain_areas(true);
-    drain_hits(true);
+  // ------------------------------------------------------------ scheduler
+  // `next_chunk(valid, id, x, depth, eidx)` loads this lane's element of the
+  // warp's next chunk and returns false (warp-uniformly) when none is left.
+  template <class ChunkFn>
+  __device__ void run(ChunkFn next_chunk) {
+    bool el_done = false;
+    for (;;) {
+      const bool up_area_empty = el_done && rg_cnt == 0;
+      const bool up_hit_empty = up_area_empty && ar_cnt == 0;
+      if (ht_cnt >= kStep || (up_hit_empty && ht_cnt > 0)) {
+        hits_step();
+      } else if (ar_cnt >= 32 || (up_area_empty && ar_cnt > 0)) {
+        areas_step();
+      } else if (rg_cnt >= 32 || (el_done && rg_cnt > 0)) {
+        regions_step();
+      } else if (!el_done) {
+        if (el_cur >= el_total) {
+          bool valid;
+          uint64_t id;
+          double x;
+          int depth;
+          uint32_t eidx;
+          if (!next_chunk(valid, id, x, depth, eidx)) {
+            el_done = true;
+          } else {
+            load_chunk(valid, id, x, depth, eidx);
+          }
+        } else {
+          element_step();
+          if (abort) return;
+        }
+      } else {
+        return;
+      }
+    }
   }
 
   __device__ double warp_full() const {

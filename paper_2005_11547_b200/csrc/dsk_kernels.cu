@@ -123,7 +123,8 @@ constexpr size_t kOffTeam = kOffQueues + kWarps * kQBytes;
 struct TeamCtl {
   long long set;
   double l1;
-  double areas;
+  double areas[2];        // per-pass area counts, double-buffered by phi parity
+  unsigned int chunk[2];  // per-pass element-chunk cursor, double-buffered
   unsigned int filled;
   int tie;
   int abort;
@@ -260,32 +261,41 @@ template <class Sink>
 __device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const PassParams &P,
                          const uint64_t *ids, const double *w, int64_t lo, int64_t nnz, int G,
                          int wit, int lane, double tf, TeamCtl &C, uint32_t &n_darts,
-                         uint32_t &n_hits, int sexp = 0) {
+                         uint32_t &n_hits, int par, int sexp = 0) {
+  int64_t next_chunk = 0;
   Engine<Sink, false> eng(T, Q, team_rwin(&C), sink, P, lane);
-  // element chunks go round-robin to the team's warps; small sets use
-  // narrower chunks so every warp of the team gets elements
+  // element chunks are handed out dynamically to the team's warps; small sets
+  // use narrower chunks so every warp of the team gets elements
   const int CH = (G == 1 || nnz >= 64 * G) ? 32 : (32 / G > 4 ? 32 / G : 4);
-  for (int64_t c = wit; c * CH < nnz; c += G) {
+  eng.run([&](bool &valid, uint64_t &id, double &x, int &depth, uint32_t &eidx) -> bool {
+    int64_t c;
+    if (G > 1) {
+      unsigned got = 0;
+      if (lane == 0) got = atomicAdd(&C.chunk[par], 1u);
+      c = __shfl_sync(DSK_FULL, got, 0);
+    } else {
+      c = next_chunk++;
+    }
+    if (c * CH >= nnz) return false;
     int64_t e = c * CH + lane;
-    bool valid = lane < CH && e < nnz;
-    uint64_t id = 0;
-    double x = 0.0;
-    int depth = 0;
+    valid = lane < CH && e < nnz;
+    id = 0;
+    x = 0.0;
+    depth = 0;
+    eidx = (uint32_t)e;
     if (valid) {
       id = ids[lo + e];
       x = w[lo + e];
       if (sexp) x = scalbn(x, sexp);
       depth = floor_log2_host(__dadd_rn(1.0, __dmul_rn(tf, x)), T.l2thr);
     }
-    eng.element_chunk(valid, id, x, depth, (uint32_t)e);
-    if (eng.abort) break;
-  }
-  if (!eng.abort) eng.finish();
+    return true;
+  });
   n_darts += eng.n_darts;
   n_hits += eng.n_hits;
   double wf = eng.warp_full();
   if (lane == 0) {
-    atomicAdd(&C.areas, wf);
+    atomicAdd(&C.areas[par], wf);
     if (eng.abort) atomicOr(&C.abort, 1);
   }
 }
@@ -328,7 +338,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) 
       slots[2 * i + 1] = 0;
     }
     if (tt == 0) {
-      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0; C.areas = 0.0;
+      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0;
+      C.areas[0] = C.areas[1] = 0.0; C.chunk[0] = C.chunk[1] = 0;
       C.darts = 0; C.hits = 0;
     }
     team_sync(G, team);
@@ -362,13 +373,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) 
         P.RD_lo = RD_prev;
         P.maxd = maxd;
         poisson_regs(P, T);
-        run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits);
+        const int par = phi & 1;
+        run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
+                 par);
         team_sync(G, team);
-        const double areas = C.areas;
+        const double areas = C.areas[par];
         const bool ab = C.abort != 0;
         const unsigned filled = C.filled;
+        // the other parity's counters were last read before the previous
+        // barrier and are next written in the following pass
+        if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
         team_sync(G, team);
-        if (tt == 0) C.areas = 0.0;
         if (ab || areas > kMaxAreas) { status = DSK_AREAS; break; }  // ref/darthash.py:243
         final_areas = areas;
         if (filled == (unsigned)k) {  // every bucket non-empty, ref/sketching.py:110
@@ -478,6 +493,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
     const double L = a.rank_limit[s];
     int status = 0;
     if (nnz == 0) status = DSK_EMPTY;                           // ref/darthash.py:133-134
+    else if (nnz >= 4096) status = DSK_TOOLARGE;  // element index field of the row sink
     else if (!(L > 0.0) || isinf(L)) status = DSK_LIMIT;        // :136-138
     int maxd = 0;
     for (int64_t i = lane; i < nnz && status == 0; i += 32) {
@@ -508,16 +524,18 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
       // the area cap is checked on a counting pass first (ref/darthash.py:242-244
       // raises before any dart is produced)
       Engine<RowSink, true> eng(T, Q, rwin, sink, P, lane);
-      for (int64_t c = 0; c * 32 < nnz; c++) {
+      int64_t next = 0;
+      eng.run([&](bool &valid, uint64_t &id, double &x, int &depth, uint32_t &eidx) -> bool {
+        int64_t c = next++;
+        if (c * 32 >= nnz) return false;
         int64_t e = c * 32 + lane;
-        bool valid = e < nnz;
-        uint64_t id = valid ? a.ids[lo + e] : 0;
-        double x = valid ? a.w[lo + e] : 0.0;
-        int depth = valid ? floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, x)), T.l2thr) : 0;
-        eng.element_chunk(valid, id, x, depth, (uint32_t)e);
-        if (eng.abort) break;
-      }
-      if (!eng.abort) eng.finish();
+        valid = e < nnz;
+        id = valid ? a.ids[lo + e] : 0;
+        x = valid ? a.w[lo + e] : 0.0;
+        depth = valid ? floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, x)), T.l2thr) : 0;
+        eidx = (uint32_t)e;
+        return true;
+      });
       if (eng.abort) status = DSK_AREAS;
     }
     __syncwarp();

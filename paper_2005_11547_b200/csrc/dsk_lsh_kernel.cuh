@@ -72,7 +72,6 @@ struct LshArgs {
   TableArgs tabs;
 };
 
-constexpr int DSK_SCRATCH = 7;  // per-set status: hit buffer overflow
 
 __host__ __device__ inline size_t lsh_team_bytes(int L) {
   return kTeamCtlBytes + align16((size_t)3 * L * sizeof(unsigned int)) + 16;
@@ -126,7 +125,8 @@ __global__ void __launch_bounds__(kWarps * 32, 1) lsh_kernel(LshArgs a) {
     const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
     for (int i = tt; i < L; i += G * 32) cnt[i] = 0;
     if (tt == 0) {
-      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0; C.areas = 0.0;
+      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0;
+      C.areas[0] = C.areas[1] = 0.0; C.chunk[0] = C.chunk[1] = 0;
       C.darts = 0; C.hits = 0; C.total = 0; C.sexp = 0; C.overflow = 0; *fullc = 0;
     }
     team_sync(G, team);
@@ -160,16 +160,17 @@ __global__ void __launch_bounds__(kWarps * 32, 1) lsh_kernel(LshArgs a) {
         P.RD_lo = RD_prev;
         P.maxd = maxd;
         poisson_regs(P, T);
+        const int par = phi & 1;
         run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
-                 sexp);
+                 par, sexp);
         team_sync(G, team);
-        const double areas = C.areas;
+        const double areas = C.areas[par];
         const bool ab = C.abort != 0;
         const unsigned total = C.total;
         const unsigned full = *fullc;
         const bool ovf = C.overflow != 0;
+        if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
         team_sync(G, team);
-        if (tt == 0) C.areas = 0.0;
         if (ab || areas > kMaxAreas) { status = DSK_AREAS; break; }  // ref/darthash.py:243
         if (ovf) { status = DSK_SCRATCH; break; }
         final_areas = areas;
