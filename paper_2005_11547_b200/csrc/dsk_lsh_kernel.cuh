@@ -206,44 +206,100 @@ __global__ void __launch_bounds__(kWarps * 32, 1) lsh_kernel(LshArgs a) {
       }
       __threadfence_block();
       team_sync(G, team);
-      // position of each entry within its bucket by (rank bits, fp); the
-      // buffer index breaks exact ties deterministically and flags them
+      // K smallest of each bucket by (rank bits, fp).  Buckets of <= 64
+      // entries (nearly all: ~2K per bucket at the stopping step) are sorted
+      // in registers with a 64-wide bitonic network; larger ones rank each
+      // entry by counting.  Bit-identical ranks with different fingerprints
+      // flag a tie (the reference orders them by index tuple).
       bool tie = false;
       for (int b = wit; b < L; b += G) {
         const unsigned o = off[b], nb = cnt[b];
-        for (unsigned i = lane; i < nb; i += 32) {
-          uint32_t ei = order[o + i];
-          ulonglong2 e = buf[ei];
-          unsigned pos = 0;
-          for (unsigned m = 0; m < nb; m++) {
-            uint32_t mi = order[o + m];
-            ulonglong2 f = buf[mi];
-            bool less = f.y < e.y || (f.y == e.y && (f.x < e.x || (f.x == e.x && mi < ei)));
-            pos += less;
-            if (f.y == e.y && mi != ei && f.x != e.x) tie = true;
+        if (nb <= 64) {
+          unsigned long long kr[2], kf[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            unsigned i = lane + 32 * h;
+            if (i < nb) {
+              ulonglong2 e = buf[order[o + i]];
+              kr[h] = e.y;
+              kf[h] = e.x;
+            } else {
+              kr[h] = ~0ULL;
+              kf[h] = ~0ULL;
+            }
           }
-          if (pos < (unsigned)K) sel[(size_t)b * K + pos] = e.x;
+          for (int kk = 2; kk <= 64; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+              if (j == 32) {  // partner of position lane is lane + 32
+                bool sw = kr[1] < kr[0] || (kr[1] == kr[0] && kf[1] < kf[0]);
+                if (sw) {
+                  unsigned long long t0 = kr[0], t1 = kf[0];
+                  kr[0] = kr[1]; kf[0] = kf[1]; kr[1] = t0; kf[1] = t1;
+                }
+              } else {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                  int p = lane + 32 * h;
+                  unsigned long long yr = __shfl_xor_sync(DSK_FULL, kr[h], j);
+                  unsigned long long yf = __shfl_xor_sync(DSK_FULL, kf[h], j);
+                  bool y_less = yr < kr[h] || (yr == kr[h] && yf < kf[h]);
+                  bool take_min = ((p & j) == 0) == ((p & kk) == 0);
+                  if (take_min == y_less) { kr[h] = yr; kf[h] = yf; }
+                }
+              }
+            }
+          }
+          // successor in sorted order (position p + 1) for the tie check
+          unsigned long long d0r = __shfl_down_sync(DSK_FULL, kr[0], 1);
+          unsigned long long d0f = __shfl_down_sync(DSK_FULL, kf[0], 1);
+          unsigned long long d1r = __shfl_down_sync(DSK_FULL, kr[1], 1);
+          unsigned long long d1f = __shfl_down_sync(DSK_FULL, kf[1], 1);
+          unsigned long long f1r = __shfl_sync(DSK_FULL, kr[1], 0);
+          unsigned long long f1f = __shfl_sync(DSK_FULL, kf[1], 0);
+          unsigned long long nxr[2] = {lane < 31 ? d0r : f1r, d1r};
+          unsigned long long nxf[2] = {lane < 31 ? d0f : f1f, d1f};
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            unsigned p = lane + 32 * h;
+            if (p + 1 < nb && nxr[h] == kr[h] && nxf[h] != kf[h]) tie = true;
+            if (p < (unsigned)K) sel[(size_t)b * K + p] = kf[h];
+          }
+        } else {
+          for (unsigned i = lane; i < nb; i += 32) {
+            uint32_t ei = order[o + i];
+            ulonglong2 e = buf[ei];
+            unsigned pos = 0;
+            for (unsigned m = 0; m < nb; m++) {
+              uint32_t mi = order[o + m];
+              ulonglong2 f = buf[mi];
+              bool less = f.y < e.y || (f.y == e.y && (f.x < e.x || (f.x == e.x && mi < ei)));
+              pos += less;
+              if (f.y == e.y && mi != ei && f.x != e.x) tie = true;
+            }
+            if (pos < (unsigned)K) sel[(size_t)b * K + pos] = e.x;
+          }
         }
       }
       if (__any_sync(DSK_FULL, tie) && lane == 0) atomicOr(&C.tie, 1);
       __threadfence_block();
       team_sync(G, team);
-      // ---- epilogue: mix64 per table (ref/randomness.py:160-166)
+      // ---- epilogue: mix64 per table (ref/randomness.py:160-166):
+      // mixed = hash64(element = v ^ mixed, w = position, stream 12)
+      const uint64_t mconst = T.tNu[0] ^ T.tRho[0] ^ __ldg(&a.tabs.tab[12 * 256]) ^
+                              __ldg(&a.tabs.tab[13 * 256]) ^ T.tR[0][0] ^ T.tR[1][0] ^
+                              __ldg(&a.tabs.tab[16 * 256]) ^ __ldg(&a.tabs.tab[17 * 256]) ^
+                              __ldg(&a.tabs.tab[18 * 256]) ^ __ldg(&a.tabs.tab[19 * 256]) ^
+                              __ldg(&a.tabs.tab[20 * 256 + kStreamKeyMix]) ^
+                              __ldg(&a.tabs.tab[21 * 256]);
       for (int b = tt; b < L; b += G * 32) {
         uint64_t mixed = 0;
         for (int p = 0; p < K; p++) {
           uint64_t v = sel[(size_t)b * K + p];
           if (a.out_fps) a.out_fps[((size_t)s * L + b) * K + p] = v;
           uint64_t e = v ^ mixed;
-          uint64_t h = 0;
+          uint64_t h = mconst ^ T.tW[0][p & 0xff] ^ T.tW[1][(p >> 8) & 0xff];
 #pragma unroll
           for (int q = 0; q < 8; q++) h ^= T.tE[q][(e >> (8 * q)) & 0xff];
-          // key fields other than element: w = p (T10, T11), stream 12
-          h ^= T.tNu[0] ^ T.tRho[0] ^ T.tW[0][p & 0xff] ^ T.tW[1][(p >> 8) & 0xff] ^
-               __ldg(&a.tabs.tab[12 * 256]) ^ __ldg(&a.tabs.tab[13 * 256]) ^ T.tR[0][0] ^
-               T.tR[1][0] ^ __ldg(&a.tabs.tab[16 * 256]) ^ __ldg(&a.tabs.tab[17 * 256]) ^
-               __ldg(&a.tabs.tab[18 * 256]) ^ __ldg(&a.tabs.tab[19 * 256]) ^
-               __ldg(&a.tabs.tab[20 * 256 + kStreamKeyMix]) ^ __ldg(&a.tabs.tab[21 * 256]);
           mixed = finalize(h);
         }
         if (a.out_keys) a.out_keys[(size_t)s * L + b] = mixed;
