@@ -42,7 +42,8 @@ constexpr int kWarps = kILP == 1 ? 24 : 12;  // warps per CTA (one CTA per SM)
 constexpr int kQR = 64 * kILP;  // region / area ring capacity (>= 31 + kStep); power of two
 constexpr int kQ = 64 * kILP;   // hit ring capacity (>= kStep - 1 + kStep); power of two
 constexpr int kJs = 64;      // folded (j, stream) table rows; Poisson counts < 64
-constexpr int kRwin = 128;   // per-pass rank-window table entries
+constexpr int kRwin = 64;    // per-pass rank-window table entries (nu, rho)
+constexpr int kRun = 8;      // areas per walker run on the direct (rho = 0) path
 
 struct SmemTables {
   uint64_t tE[8][256];    // T0..T7  element bytes
@@ -67,6 +68,7 @@ struct WarpQueues {
   uint4 arB[kQR];       //         {w, r, meta, element index (materialising sink)}
   ulonglong2 ht[kQ];    // hit:    {P_A ^ js[j][fp], rank bits}
   ulonglong2 el[32];    // element chunk: {E, x}
+  uint2 elD[32];        // direct path: {rho=0 areas of the element, top nu | first V nu << 8}
   uint32_t elIdx[32];
 };
 
@@ -159,21 +161,30 @@ template <class Sink, bool kFull>
 struct Engine {
   const SmemTables &T;
   WarpQueues &Q;
-  uint2 *rwin;          // per-pass rank windows by (nu, rho): {r_hi + 1, r_lo | hasprev << 31}
+  // per-pass rank windows by (nu, rho): {r_hi + 1, r_lo | hasprev << 31,
+  // inclusive prefix over nu of rho=0 in-band areas, inclusive prefix of
+  // rho=0 full-step areas}
+  uint4 *rwin;
   Sink &sink;
-  const PassParams P;
+  const PassParams &P;  // in shared memory: read on use instead of pinning ~20 registers
   int lane;
   int rg_head = 0, rg_cnt = 0, ar_head = 0, ar_cnt = 0, ht_head = 0, ht_cnt = 0;
   uint32_t rg_cur = 0, ar_cur = 0;
   bool use_table = false;
+  bool direct = false;      // rho = 0 areas come from per-lane walkers, not the region ring
   bool abort = false;       // warp-uniform: area cap exceeded by one lane's share
   double lane_full = 0.0;   // per lane: areas of the full (non-band) step (area cap)
   uint32_t n_darts = 0;     // per lane: candidate darts first seen in this band
   uint32_t n_hits = 0;      // per lane
   // element chunk state: lane i holds element i's region-count scan
   uint32_t el_excl = 0, el_total = 0, el_cur = 0;
+  // direct path: chunk run scan (lane i: element i's first run) and cursor
+  uint32_t run_excl = 0, run_total = 0, run_cur = 0;
+  // direct path walker of this lane: areas [wk_a, wk_end) of element wk_slot
+  uint32_t wk_a = 0, wk_end = 0, wk_r = 0, wk_rhi = 0, wk_rlo = 0;
+  int wk_slot = 0, wk_nu = 0;
 
-  __device__ Engine(const SmemTables &t, WarpQueues &q, uint2 *rw, Sink &s, const PassParams &p,
+  __device__ Engine(const SmemTables &t, WarpQueues &q, uint4 *rw, Sink &s, const PassParams &p,
                     int ln)
       : T(t), Q(q), rwin(rw), sink(s), P(p), lane(ln) {
     // rank windows depend on (nu, rho, limit) only: tabulate them per pass
@@ -194,8 +205,35 @@ struct Engine {
         // r_hi <= 2^27 whenever the step is legal; larger values saturate and
         // the area cap rejects the step
         uint32_t hi1 = r_hi < 0 ? 0u : (r_hi >= 0x7fffffff ? 0x7fffffffu : (uint32_t)r_hi + 1);
-        rwin[e] = make_uint2(hi1, lo);  // team warps write identical values
+        // team warps write identical values into every field, and each warp
+        // writes the whole table before reading it: no transient values
+        reinterpret_cast<uint2 *>(&rwin[e])[0] = make_uint2(hi1, lo);
       }
+      __syncwarp();
+      // direct path tables: prefix sums over nu of the rho = 0 row counts
+      uint32_t carry_a = 0, carry_f = 0;
+      bool narrow = true;
+      for (int nu0 = 0; nu0 <= P.maxd; nu0 += 32) {
+        int nu = nu0 + lane;
+        uint32_t ca = 0, cf = 0;
+        if (nu <= P.maxd) {
+          uint4 rw = rwin[nu * rdp1];
+          uint32_t hi1 = rw.x, rlo = rw.y & 0x7fffffffu;
+          cf = hi1;                                 // r_hi + 1 rows in the full step
+          ca = hi1 > rlo ? hi1 - rlo : 0;           // rows r_lo .. r_hi in this band
+          narrow = narrow && hi1 <= 65536;
+        }
+        uint32_t ia = warp_incl_scan(ca, lane) + carry_a;
+        uint32_t fi = warp_incl_scan(cf, lane) + carry_f;
+        if (nu <= P.maxd) reinterpret_cast<uint2 *>(&rwin[nu * rdp1])[1] = make_uint2(ia, fi);
+        carry_a = __shfl_sync(DSK_FULL, ia, 31);
+        carry_f = __shfl_sync(DSK_FULL, fi, 31);
+      }
+      // row counts stay far below 2^31 for every legal step
+      // (sets with rank depth >= 1 have few areas per rho = 0 row: the region
+      // ring expands them more cheaply than short walker runs)
+      direct = P.RD == 0 && __all_sync(DSK_FULL, narrow) && carry_a < (1u << 30) &&
+               carry_f < (1u << 30);
     }
     __syncwarp();
   }
@@ -432,15 +470,124 @@ struct Engine {
 #pragma unroll
       for (int p = 0; p < 8; p++) E ^= T.tE[p][(id >> (8 * p)) & 0xff];
     }
+    uint32_t c;
+    uint32_t nruns = 0, cnt0 = 0, dmeta = 0;
+    if (direct) {
+      // rho = 0 regions (nu, 0) have w_hi = 0 iff w0[nu] <= x (wmax = 0); w0
+      // grows with nu, so they are exactly nu <= dtop.  Column 0 is the w_hi
+      // column; its darts can miss only where the region's upper weight edge
+      // fl(w0 + fl(1 * dnu)) exceeds x, i.e. from nu_v up (edges grow with nu).
+      int dtop = valid ? depth : -1;
+      while (dtop >= 0 && T.w0[dtop] > x) dtop--;
+      int nu_v = dtop + 1;
+      while (nu_v > 0 && __dadd_rn(T.w0[nu_v - 1], __dmul_rn(P.inv_t, pow2(nu_v - 1))) > x) nu_v--;
+      if (dtop >= 0) {
+        uint4 rw = rwin[dtop * (P.RD + 1)];
+        cnt0 = rw.z;
+        lane_full += (double)rw.w;
+      }
+      nruns = (cnt0 + kRun - 1) / kRun;
+      dmeta = (uint32_t)(dtop & 0xff) | ((uint32_t)nu_v << 8);
+      c = valid ? (uint32_t)(depth + 1) * (uint32_t)P.RD : 0;  // rho >= 1 regions
+    } else {
+      c = valid ? (uint32_t)(depth + 1) * (uint32_t)(P.RD + 1) : 0;
+    }
     __syncwarp();
     Q.el[lane] = make_ulonglong2(E, (unsigned long long)__double_as_longlong(x));
+    Q.elD[lane] = make_uint2(cnt0, dmeta);
     if (kFull) Q.elIdx[lane] = eidx;
     __syncwarp();
-    uint32_t c = valid ? (uint32_t)(depth + 1) * (uint32_t)(P.RD + 1) : 0;
     uint32_t incl = warp_incl_scan(c, lane);
     el_total = __shfl_sync(DSK_FULL, incl, 31);
     el_excl = incl - c;
     el_cur = 0;
+    uint32_t rincl = warp_incl_scan(nruns, lane);
+    run_total = __shfl_sync(DSK_FULL, rincl, 31);
+    run_excl = rincl - nruns;
+    run_cur = 0;
+  }
+
+  // ------------------------------------------------------- direct (rho = 0)
+  // Each lane walks a run of <= kRun consecutive rho = 0 areas of one element
+  // (nu ascending, r ascending: the same areas the region ring would yield,
+  // in any order), one area per step; idle lanes take the chunk's next runs.
+  __device__ __forceinline__ void walker_seek(uint32_t a, int dtop) {
+    // smallest nu <= dtop with inclusive prefix > a
+    const int rdp1 = P.RD + 1;
+    int lo = 0, hi = dtop;
+    while (lo < hi) {
+      int mid = (lo + hi) >> 1;
+      if (rwin[mid * rdp1].z > a) hi = mid; else lo = mid + 1;
+    }
+    uint4 rw = rwin[lo * rdp1];
+    uint32_t rows = rw.x > (rw.y & 0x7fffffffu) ? rw.x - (rw.y & 0x7fffffffu) : 0;
+    wk_nu = lo;
+    wk_rlo = rw.y;
+    wk_rhi = rw.x - 1;
+    wk_r = (rw.y & 0x7fffffffu) + (a - (rw.z - rows));
+  }
+
+  __device__ void direct_step() {
+    // refill idle walkers with the chunk's next runs
+    bool idle = wk_a >= wk_end;
+    unsigned idle_mask = __ballot_sync(DSK_FULL, idle);
+    if (run_cur < run_total && __popc(idle_mask) >= 8 || idle_mask == DSK_FULL) {
+      uint32_t q = run_cur + __popc(idle_mask & ((1u << lane) - 1));
+      int src = warp_owner(run_excl, q);
+      uint32_t first = __shfl_sync(DSK_FULL, run_excl, src);
+      if (idle && q < run_total) {
+        uint2 d = Q.elD[src];
+        uint32_t a0 = (q - first) * kRun;
+        wk_slot = src;
+        wk_a = a0;
+        wk_end = a0 + kRun < d.x ? a0 + kRun : d.x;
+        walker_seek(a0, (int)(d.y & 0xff));
+      }
+      uint32_t took = (uint32_t)__popc(idle_mask);
+      run_cur = run_cur + took < run_total ? run_cur + took : run_total;
+    }
+    const bool act = wk_a < wk_end;
+    ulonglong2 el = Q.el[wk_slot];
+    uint2 d = Q.elD[wk_slot];
+    const int nu = wk_nu;
+    const uint32_t r = wk_r;
+    uint64_t p = el.x ^ T.tNu[nu] ^ T.tRho[0] ^ T.tW[0][0] ^ T.tW[1][0] ^ T.cfold ^
+                 T.tR[0][r & 0xff] ^ T.tR[1][(r >> 8) & 0xff];
+    uint32_t k = poisson_count(finalize(p ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
+    uint32_t cnt = act ? k : 0;
+    const bool hp = (wk_rlo & 0x80000000u) != 0;
+    const bool lb = hp && r == (wk_rlo & 0x7fffffffu);
+    if (!lb) n_darts += cnt;
+    uint32_t meta = (uint32_t)nu | (cnt << 16) | (nu >= (int)(d.y >> 8) ? kArWb : 0) |
+                    (r == wk_rhi ? kArRb : 0) | (lb ? kArLb : 0);
+    push_area(cnt > 0, p, __longlong_as_double((long long)el.y), 0, r, meta,
+              kFull ? Q.elIdx[wk_slot] : 0);
+    // advance: next row, else the next non-empty nu
+    if (act) {
+      wk_a++;
+      if (wk_a < wk_end) {
+        if (r < wk_rhi) {
+          wk_r = r + 1;
+        } else {
+          const int rdp1 = P.RD + 1;
+          int nn = nu + 1;
+          uint4 rw = rwin[nn * rdp1];
+          while (rw.x <= (rw.y & 0x7fffffffu)) {  // empty band row range
+            nn++;
+            rw = rwin[nn * rdp1];
+          }
+          wk_nu = nn;
+          wk_rlo = rw.y;
+          wk_rhi = rw.x - 1;
+          wk_r = rw.y & 0x7fffffffu;
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  __device__ __forceinline__ bool walkers_busy() const {
+    return __any_sync(DSK_FULL, wk_a < wk_end) || run_cur < run_total;
   }
 
   // regions [el_cur, el_cur + 64) of the element chunk: the surviving
@@ -448,6 +595,7 @@ struct Engine {
   __device__ void element_step() {
     const int rdp1 = P.RD + 1;
     const float inv_rdp1 = 1.0f / (float)rdp1;
+    const float inv_rd = P.RD > 0 ? 1.0f / (float)P.RD : 0.0f;
     const uint32_t lo = el_cur, hi = lo + kStep < el_total ? lo + kStep : el_total;
     bool ok[kILP];
     uint64_t pr[kILP];
@@ -460,7 +608,14 @@ struct Engine {
       int src = warp_owner(el_excl, pos);
       uint32_t idx = pos - __shfl_sync(DSK_FULL, el_excl, src);
       int nu, rho;
-      if (rdp1 == 1) {
+      if (direct) {  // rho = 0 comes from the walkers: idx covers rho in [1, RD]
+        const int rd = P.RD;
+        nu = (int)(((float)idx + 0.5f) * inv_rd);
+        rho = (int)idx - nu * rd;
+        if (rho < 0) { nu--; rho += rd; }
+        else if (rho >= rd) { nu++; rho -= rd; }
+        rho += 1;
+      } else if (rdp1 == 1) {
         nu = (int)idx;
         rho = 0;
       } else {  // fp32 quotient, off by at most one: corrected below
@@ -479,7 +634,7 @@ struct Engine {
         int64_t r_hi, r_lo = 0;
         uint32_t flags = 0;
         if (use_table) {
-          uint2 rw = rwin[nu * rdp1 + rho];
+          uint4 rw = rwin[nu * rdp1 + rho];
           r_hi = (int64_t)rw.x - 1;
           if (rw.y & 0x80000000u) { r_lo = rw.y & 0x7fffffffu; flags |= kRgHasPrev >> 16; }
         } else {
@@ -545,7 +700,12 @@ struct Engine {
       } else if (rg_cnt >= 32 || (el_done && rg_cnt > 0)) {
         regions_step();
       } else if (!el_done) {
-        if (el_cur >= el_total) {
+        if (direct && walkers_busy()) {
+          direct_step();
+        } else if (el_cur < el_total) {
+          element_step();
+          if (abort) return;
+        } else {
           bool valid;
           uint64_t id;
           double x;
@@ -555,10 +715,11 @@ struct Engine {
             el_done = true;
           } else {
             load_chunk(valid, id, x, depth, eidx);
+            if (__any_sync(DSK_FULL, lane_full > kMaxAreas)) {  // direct rows' cap share
+              abort = true;
+              return;
+            }
           }
-        } else {
-          element_step();
-          if (abort) return;
         }
       } else {
         return;

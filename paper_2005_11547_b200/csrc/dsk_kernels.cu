@@ -135,11 +135,12 @@ struct TeamCtl {
   int sexp;       // weight rescaling exponent (LSH normalisation), 0 otherwise
   unsigned int total;  // LSH: buffered hits
   int overflow;        // LSH: hit buffer overflow
+  PassParams pp;       // parameters of the current pass (identical writes by the team's warps)
 };
 // per-team block: control word + the per-pass rank-window table
-constexpr size_t kTeamCtlBytes = align16(sizeof(TeamCtl)) + kRwin * sizeof(uint2);
-__device__ __forceinline__ uint2 *team_rwin(TeamCtl *C) {
-  return reinterpret_cast<uint2 *>(reinterpret_cast<unsigned char *>(C) + align16(sizeof(TeamCtl)));
+constexpr size_t kTeamCtlBytes = align16(sizeof(TeamCtl)) + kRwin * sizeof(uint4);
+__device__ __forceinline__ uint4 *team_rwin(TeamCtl *C) {
+  return reinterpret_cast<uint4 *>(reinterpret_cast<unsigned char *>(C) + align16(sizeof(TeamCtl)));
 }
 
 __device__ __forceinline__ void team_sync(int G, int team) {
@@ -263,7 +264,9 @@ __device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const P
                          int wit, int lane, double tf, TeamCtl &C, uint32_t &n_darts,
                          uint32_t &n_hits, int par, int sexp = 0) {
   int64_t next_chunk = 0;
-  Engine<Sink, false> eng(T, Q, team_rwin(&C), sink, P, lane);
+  C.pp = P;
+  __syncwarp();
+  Engine<Sink, false> eng(T, Q, team_rwin(&C), sink, C.pp, lane);
   // element chunks are handed out dynamically to the team's warps; small sets
   // use narrower chunks so every warp of the team gets elements
   const int CH = (G == 1 || nnz >= 64 * G) ? 32 : (32 / G > 4 ? 32 / G : 4);
@@ -485,8 +488,12 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
   unsigned long long *cursors =
       reinterpret_cast<unsigned long long *>(smem + kOffTeam);
-  uint2 *rwin = reinterpret_cast<uint2 *>(smem + kOffTeam + kWarps * sizeof(unsigned long long)) +
+  uint4 *rwin = reinterpret_cast<uint4 *>(smem + kOffTeam +
+                                          align16(kWarps * sizeof(unsigned long long))) +
                 warp * kRwin;
+  PassParams *pps = reinterpret_cast<PassParams *>(
+      smem + kOffTeam + align16(kWarps * sizeof(unsigned long long)) +
+      kWarps * kRwin * sizeof(uint4));
   __syncthreads();
   for (int64_t s = (int64_t)blockIdx.x * kWarps + warp; s < a.n; s += (int64_t)gridDim.x * kWarps) {
     const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
@@ -523,7 +530,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
       sink.cursor = &cursors[warp];
       // the area cap is checked on a counting pass first (ref/darthash.py:242-244
       // raises before any dart is produced)
-      Engine<RowSink, true> eng(T, Q, rwin, sink, P, lane);
+      if (lane == 0) pps[warp] = P;
+      __syncwarp();
+      Engine<RowSink, true> eng(T, Q, rwin, sink, pps[warp], lane);
       int64_t next = 0;
       eng.run([&](bool &valid, uint64_t &id, double &x, int &depth, uint32_t &eidx) -> bool {
         int64_t c = next++;
@@ -750,7 +759,8 @@ extern "C" int dsk_darts_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *
   a.counts = counts; a.status = status; a.element = element; a.nu = nu; a.rho = rho; a.ww = w;
   a.rr = r; a.jj = j; a.weight = weight; a.rank = rank; a.fp = fingerprint;
   a.tabs = table_args(c, (double)t);
-  size_t smem = kOffTeam + kWarps * (sizeof(unsigned long long) + kRwin * sizeof(uint2));
+  size_t smem = kOffTeam + align16(kWarps * sizeof(unsigned long long)) +
+                kWarps * kRwin * sizeof(uint4) + kWarps * sizeof(PassParams);
   int grid = (int)((n + kWarps - 1) / kWarps);
   if (grid > c->num_sms) grid = c->num_sms;
   darts_kernel<<<grid, kWarps * 32, smem, st>>>(a);
