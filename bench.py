@@ -61,8 +61,19 @@ def dist_env():
 
 
 def workload_rows(cfg, rank, n_per_rank):
+    """CSR rows of this rank (optionally cached as .npy under $DSK_WL_CACHE)."""
     from paper_2005_11547_b200 import workloads
-    return workloads.generate(cfg.name, n=n_per_rank, start=rank * n_per_rank)
+    cache = os.environ.get("DSK_WL_CACHE")
+    if cache:
+        base = os.path.join(cache, f"{cfg.name}_{rank * n_per_rank}_{n_per_rank}")
+        if os.path.exists(base + "_w.npy"):
+            return (np.load(base + "_p.npy"), np.load(base + "_i.npy"), np.load(base + "_w.npy"))
+    out = workloads.generate(cfg.name, n=n_per_rank, start=rank * n_per_rank)
+    if cache:
+        os.makedirs(cache, exist_ok=True)
+        for suffix, arr in zip(("_p", "_i", "_w"), out):
+            np.save(base + suffix + ".npy", arr)
+    return out
 
 
 class ClockSampler:

@@ -16,7 +16,7 @@ import threading
 PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB_PATH = os.path.join(PKG, "libdsk_b200.so")
+LIB_PATH = os.environ.get("DSK_LIB_PATH") or os.path.join(PKG, "libdsk_b200.so")
 HEADER = os.path.join(REPO, "include", "dsk_b200.h")
 SOURCES = ["dsk_kernels.cu", "dsk_device.cuh", "dsk_engine.cuh", "dsk_lsh_kernel.cuh",
            "dsk_lsh_host.cuh"]
@@ -48,20 +48,26 @@ def needs_build() -> bool:
     return any(os.path.exists(d) and os.path.getmtime(d) > mtime for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    """Compile csrc/dsk_kernels.cu into libdsk_b200.so for sm_100a."""
+def build(force: bool = False, verbose: bool = False, out: str | None = None,
+          defines: dict | None = None) -> str:
+    """Compile csrc/dsk_kernels.cu into libdsk_b200.so for sm_100a.
+
+    `out`/`defines` build a tuning variant (see profiles/sweep.py) instead.
+    """
     with _lock:
-        if not force and not needs_build():
+        target = out or LIB_PATH
+        if out is None and not force and not needs_build():
             return LIB_PATH
-        tmp = LIB_PATH + ".tmp"
-        cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, os.path.join(CSRC, "dsk_kernels.cu")]
+        tmp = target + ".tmp"
+        dflags = [f"-D{k}={v}" for k, v in (defines or {}).items()]
+        cmd = [_nvcc(), *NVCC_FLAGS, *dflags, "-o", tmp, os.path.join(CSRC, "dsk_kernels.cu")]
         res = subprocess.run(cmd, cwd=CSRC, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError("nvcc failed:\n" + res.stdout + res.stderr)
         if verbose:
             print(res.stdout + res.stderr)
-        os.replace(tmp, LIB_PATH)
-        return LIB_PATH
+        os.replace(tmp, target)
+        return target
 
 
 # (name, restype, argtypes)

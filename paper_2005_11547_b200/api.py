@@ -87,7 +87,10 @@ def _to_dev(a, dtype: torch.dtype, device: torch.device) -> torch.Tensor:
         arr = arr.astype(np.int64, copy=False)
     elif dtype == torch.float64:
         arr = arr.astype(np.float64, copy=False)
-    return torch.from_numpy(np.ascontiguousarray(arr)).to(device)
+    arr = np.ascontiguousarray(arr)
+    if not arr.flags.writeable:
+        arr = arr.copy()
+    return torch.from_numpy(arr).to(device)
 
 
 def as_u64(t: torch.Tensor) -> np.ndarray:

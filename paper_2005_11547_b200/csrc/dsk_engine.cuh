@@ -36,14 +36,28 @@
 
 namespace dsk {
 
+// build-time tunables (profiles/sweep.sh builds variants)
+#ifndef DSK_WARPS
+#define DSK_WARPS 24
+#endif
+#ifndef DSK_RUN
+#define DSK_RUN 4
+#endif
+#ifndef DSK_DIRECT
+#define DSK_DIRECT 1
+#endif
+#ifndef DSK_REFILL
+#define DSK_REFILL 8
+#endif
+
 constexpr int kILP = 1;      // children per lane per stage step (independent chains)
 constexpr int kStep = 32 * kILP;
-constexpr int kWarps = kILP == 1 ? 24 : 12;  // warps per CTA (one CTA per SM)
+constexpr int kWarps = DSK_WARPS;  // warps per CTA (one CTA per SM)
 constexpr int kQR = 64 * kILP;  // region / area ring capacity (>= 31 + kStep); power of two
 constexpr int kQ = 64 * kILP;   // hit ring capacity (>= kStep - 1 + kStep); power of two
 constexpr int kJs = 64;      // folded (j, stream) table rows; Poisson counts < 64
 constexpr int kRwin = 64;    // per-pass rank-window table entries (nu, rho)
-constexpr int kRun = 8;      // areas per walker run on the direct (rho = 0) path
+constexpr int kRun = DSK_RUN;  // areas per walker run on the direct (rho = 0) path
 
 struct SmemTables {
   uint64_t tE[8][256];    // T0..T7  element bytes
@@ -232,7 +246,7 @@ struct Engine {
       // row counts stay far below 2^31 for every legal step
       // (sets with rank depth >= 1 have few areas per rho = 0 row: the region
       // ring expands them more cheaply than short walker runs)
-      direct = P.RD == 0 && __all_sync(DSK_FULL, narrow) && carry_a < (1u << 30) &&
+      direct = DSK_DIRECT && P.RD == 0 && __all_sync(DSK_FULL, narrow) && carry_a < (1u << 30) &&
                carry_f < (1u << 30);
     }
     __syncwarp();
@@ -531,7 +545,7 @@ struct Engine {
     // refill idle walkers with the chunk's next runs
     bool idle = wk_a >= wk_end;
     unsigned idle_mask = __ballot_sync(DSK_FULL, idle);
-    if (run_cur < run_total && __popc(idle_mask) >= 8 || idle_mask == DSK_FULL) {
+    if ((run_cur < run_total && __popc(idle_mask) >= DSK_REFILL) || idle_mask == DSK_FULL) {
       uint32_t q = run_cur + __popc(idle_mask & ((1u << lane) - 1));
       int src = warp_owner(run_excl, q);
       uint32_t first = __shfl_sync(DSK_FULL, run_excl, src);

@@ -119,6 +119,10 @@ __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(siz
 constexpr size_t kOffQueues = align16(sizeof(SmemTables));
 constexpr size_t kQBytes = align16(sizeof(WarpQueues));
 constexpr size_t kOffTeam = kOffQueues + kWarps * kQBytes;
+// minhash / LSH kernels are instantiated for several CTA widths (warps per
+// CTA); the host picks per launch the width whose team size is smallest.
+__host__ __device__ constexpr size_t off_team(int nw) { return kOffQueues + nw * kQBytes; }
+constexpr int kWidths[] = {24, 22, 20};
 
 struct TeamCtl {
   long long set;
@@ -310,7 +314,8 @@ __device__ __forceinline__ void poisson_regs(PassParams &P, const SmemTables &T)
   P.pt3 = T.pthr[3];
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) {
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
   load_tables(T, a.tabs);
@@ -318,9 +323,9 @@ __global__ void __launch_bounds__(kWarps * 32, 1) minhash_kernel(MinhashArgs a) 
   const int G = a.G, team = warp / G, wit = warp % G, tt = wit * 32 + lane;
   const int k = a.k;
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
-  TeamCtl &C = *reinterpret_cast<TeamCtl *>(smem + kOffTeam + team * kTeamCtlBytes);
-  const int teams = kWarps / G;
-  uint64_t *slots = reinterpret_cast<uint64_t *>(smem + kOffTeam + teams * kTeamCtlBytes) +
+  TeamCtl &C = *reinterpret_cast<TeamCtl *>(smem + off_team(NW) + team * kTeamCtlBytes);
+  const int teams = NW / G;
+  uint64_t *slots = reinterpret_cast<uint64_t *>(smem + off_team(NW) + teams * kTeamCtlBytes) +
                     (size_t)team * 2 * k;
   __syncthreads();
 
@@ -633,9 +638,9 @@ __global__ void __launch_bounds__(512) hash_peak_kernel(const uint64_t *tab, int
 
 // ------------------------------------------------------------- host side
 
-static size_t minhash_smem(int k, int G) {
-  int teams = kWarps / G;
-  return kOffTeam + teams * kTeamCtlBytes + (size_t)teams * k * 16;
+static size_t minhash_smem(int k, int G, int nw) {
+  int teams = nw / G;
+  return off_team(nw) + teams * kTeamCtlBytes + (size_t)teams * k * 16;
 }
 
 extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const double *cdf_host,
@@ -662,11 +667,19 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
   CUDA_TRY(cudaMemcpy(c->d_tab, tables_host, 22 * 256 * sizeof(uint64_t), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c->d_pthr, pthr, sizeof(pthr), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c->d_l2thr, log2_thr_host, 258 * sizeof(double), cudaMemcpyHostToDevice));
-  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<22>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(darts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
-  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<22>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
   *out = c;
   return DSK_OK;
@@ -700,12 +713,26 @@ static TableArgs table_args(const dsk_ctx *c, double tf) {
   return t;
 }
 
-// smallest team (warps per set) whose slot arrays fit beside the queues
-static int choose_team(const dsk_ctx *c, int k) {
-  static const int kTeams[] = {1, 2, 3, 4, 6, 8, 12, 24};
-  for (int G : kTeams)
-    if (minhash_smem(k, G) <= c->max_smem) return G;
-  return -1;
+// a team size must divide the CTA's warps; teams of > 1 warp synchronise on
+// named barriers 1..15
+static bool team_size_ok(int G, int nw) { return nw % G == 0 && (G == 1 || nw / G <= 15); }
+
+// (CTA width, team size): the smallest team whose slot arrays fit beside the
+// queues, preferring the wider CTA on ties
+template <class SmemFn>
+static bool choose_shape(const dsk_ctx *c, SmemFn smem_of, int &nw_out, int &g_out) {
+  int best_g = 1 << 30, best_nw = 0;
+  for (int nw : kWidths) {
+    for (int G = 1; G <= nw; G++) {
+      if (!team_size_ok(G, nw) || smem_of(G, nw) > c->max_smem) continue;
+      if (G < best_g) { best_g = G; best_nw = nw; }
+      break;
+    }
+  }
+  if (!best_nw) return false;
+  nw_out = best_nw;
+  g_out = best_g;
+  return true;
 }
 
 extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
@@ -717,8 +744,9 @@ extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
   if (n == 0) return DSK_OK;
   int64_t t = dsk_minhash_density(k);
   if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "k too large");
-  int G = choose_team(c, k);
-  if (G < 0) return set_err(DSK_EUNSUPPORTED, "k too large for the shared-memory slot array");
+  int NW = 0, G = 0;
+  if (!choose_shape(c, [&](int g, int nw) { return minhash_smem(k, g, nw); }, NW, G))
+    return set_err(DSK_EUNSUPPORTED, "k too large for the shared-memory slot array");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
   // each launch owns one counter slot; slots recycle after kCounterSlots launches,
@@ -730,10 +758,14 @@ extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
   a.tf = (double)t; a.inv_t = 1.0 / (double)t; a.md = make_mod((uint32_t)k); a.G = G;
   a.out_values = out_values; a.out_bits = out_bits; a.status = status; a.phi = phi;
   a.stats = stats; a.counter = counter; a.tabs = table_args(c, (double)t);
-  size_t smem = minhash_smem(k, G);
+  size_t smem = minhash_smem(k, G, NW);
   int grid = c->num_sms;
-  if ((int64_t)grid * (kWarps / G) > n) grid = (int)((n + (kWarps / G) - 1) / (kWarps / G));
-  minhash_kernel<<<grid, kWarps * 32, smem, st>>>(a);
+  if ((int64_t)grid * (NW / G) > n) grid = (int)((n + (NW / G) - 1) / (NW / G));
+  switch (NW) {
+    case 24: minhash_kernel<24><<<grid, 24 * 32, smem, st>>>(a); break;
+    case 22: minhash_kernel<22><<<grid, 22 * 32, smem, st>>>(a); break;
+    default: minhash_kernel<20><<<grid, 20 * 32, smem, st>>>(a); break;
+  }
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
 }

@@ -1,12 +1,5 @@
 // dsk_lsh_host.cuh -- host side of K5 (included at the end of dsk_kernels.cu).
 
-static int choose_lsh_team(const dsk_ctx *c, int L) {
-  static const int kTeams[] = {1, 2, 3, 4, 6, 8, 12, 24};
-  for (int G : kTeams)
-    if (lsh_smem(L, G) <= c->max_smem) return G;
-  return -1;
-}
-
 extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                            const double *weights, int64_t n, int32_t L, int32_t K,
                            int32_t normalize, uint64_t *out_keys, uint64_t *out_fps,
@@ -16,11 +9,12 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   if (n == 0) return DSK_OK;
   int64_t t = (int64_t)L * K;
   if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "L*K too large");
-  int G = choose_lsh_team(c, L);
-  if (G < 0) return set_err(DSK_EUNSUPPORTED, "L too large for the shared-memory bucket counters");
+  int NW = 0, G = 0;
+  if (!choose_shape(c, [&](int g, int nw) { return lsh_smem(L, g, nw); }, NW, G))
+    return set_err(DSK_EUNSUPPORTED, "L too large for the shared-memory bucket counters");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
-  const int teams = kWarps / G;
+  const int teams = NW / G;
   int grid = c->num_sms;
   if ((int64_t)grid * teams > n) grid = (int)((n + teams - 1) / teams);
   // hit buffer per team: ~8 phi steps of L*K darts, at least 16K entries
@@ -46,7 +40,11 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
   a.scratch = (unsigned char *)c->lsh_scratch; a.team_scratch = team_bytes; a.cap = cap;
   a.tabs = table_args(c, (double)t);
-  lsh_kernel<<<grid, kWarps * 32, lsh_smem(L, G), st>>>(a);
+  switch (NW) {
+    case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+    case 22: lsh_kernel<22><<<grid, 22 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+    default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+  }
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
 }

@@ -77,12 +77,13 @@ __host__ __device__ inline size_t lsh_team_bytes(int L) {
   return kTeamCtlBytes + align16((size_t)3 * L * sizeof(unsigned int)) + 16;
 }
 
-__host__ __device__ inline size_t lsh_smem(int L, int G) {
-  int teams = kWarps / G;
-  return kOffTeam + (size_t)teams * lsh_team_bytes(L);
+__host__ __device__ inline size_t lsh_smem(int L, int G, int nw) {
+  int teams = nw / G;
+  return off_team(nw) + (size_t)teams * lsh_team_bytes(L);
 }
 
-__global__ void __launch_bounds__(kWarps * 32, 1) lsh_kernel(LshArgs a) {
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
   load_tables(T, a.tabs);
@@ -90,7 +91,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) lsh_kernel(LshArgs a) {
   const int G = a.G, team = warp / G, wit = warp % G, tt = wit * 32 + lane;
   const int L = a.L, K = a.K;
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
-  unsigned char *tb = smem + kOffTeam + team * lsh_team_bytes(L);
+  unsigned char *tb = smem + off_team(NW) + team * lsh_team_bytes(L);
   TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
   unsigned int *cnt = reinterpret_cast<unsigned int *>(tb + kTeamCtlBytes);
   unsigned int *off = cnt + L;
@@ -98,7 +99,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) lsh_kernel(LshArgs a) {
   unsigned int *fullc = reinterpret_cast<unsigned int *>(tb + kTeamCtlBytes +
                                                          align16((size_t)3 * L * sizeof(unsigned)));
   // global scratch of this team
-  const int teams = kWarps / G;
+  const int teams = NW / G;
   unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
   ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
   uint32_t *bkt = reinterpret_cast<uint32_t *>(gs + (size_t)a.cap * 16);
