@@ -134,6 +134,19 @@ int dsk_pack_onebit(const uint64_t *values, int64_t n, int32_t k, uint64_t *out_
 int dsk_hash_peak(dsk_ctx *ctx, int64_t n_per_thread, uint64_t *sink, int64_t *hashes_done,
                   void *stream);
 
+/* float(np.sum(weights)) of every set (ref/core.py:44, numpy pairwise order):
+ * the denominator of each phi step's rank limit phi / ||x||_1. */
+int dsk_l1_csr(const int64_t *indptr, const double *weights, int64_t n, double *out_l1,
+               void *stream);
+
+/* DSK1 records (ref/sketching.py:210-231) for n sketches, byte-identical to
+ * b"".join(dump_sketch(s) for s in sketches): kind 1 = minhash (payload k
+ * uint64 values per set), 2 = one-bit (payload: the packed words of
+ * dsk_minhash_csr's out_bits, ceil(k/8) bytes written), 3 = bottom-k
+ * fingerprints (k uint64).  out holds n * (20 + payload bytes). */
+int dsk_dsk1_records(int32_t kind, int32_t k, uint64_t seed, const uint64_t *payload, int64_t n,
+                     uint8_t *out, void *stream);
+
 const char *dsk_last_error(void);
 
 #ifdef __cplusplus

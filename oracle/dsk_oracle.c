@@ -356,6 +356,42 @@ int or_minhash(const uint64_t *tab, const double *cdf, const uint64_t *ids, cons
   return status;
 }
 
+/* ref/sketching.py:146-156: density t = k; at the first phi with >= k darts,
+ * the k smallest darts by (rank, index) (_bottom_indices :126-143), ascending. */
+static __thread const or_dart *t_bk_darts;
+static int bk_cmp(const void *pa, const void *pb) {
+  const or_dart *a = &t_bk_darts[*(const int64_t *)pa], *b = &t_bk_darts[*(const int64_t *)pb];
+  if (dart_less(a, b)) return -1;
+  if (dart_less(b, a)) return 1;
+  return 0;
+}
+
+int or_bottom_k(const uint64_t *tab, const double *cdf, const uint64_t *ids, const double *x,
+                int64_t n, double l1, int64_t k, or_dart *out, int32_t *phi_out) {
+  if (n == 0) return OR_EMPTY;
+  if (k < 1) return OR_BADARG;
+  or_dart_vec dv = {0};
+  int status = OR_NOCONV;
+  for (int phi = 1; phi <= MAX_PHI_STEPS; phi++) {
+    dv.size = 0;
+    int st = or_dart_batch(tab, cdf, k, ids, x, n, (double)phi / l1, &dv);
+    if (st != OR_OK) { status = st; break; }
+    if (dv.size < k) continue;
+    int64_t *idx = (int64_t *)malloc((size_t)dv.size * sizeof(int64_t));
+    if (!idx) { status = OR_NOMEM; break; }
+    for (int64_t i = 0; i < dv.size; i++) idx[i] = i;
+    t_bk_darts = dv.data;
+    qsort(idx, (size_t)dv.size, sizeof(int64_t), bk_cmp);
+    for (int64_t i = 0; i < k; i++) out[i] = dv.data[idx[i]];
+    free(idx);
+    if (phi_out) *phi_out = phi;
+    status = OR_OK;
+    break;
+  }
+  or_dart_vec_free(&dv);
+  return status;
+}
+
 typedef struct {
   int64_t idx;
   int64_t bucket;

@@ -55,6 +55,8 @@ int or_minhash(const uint64_t *tab, const double *cdf, const uint64_t *ids, cons
 int or_lsh_key(const uint64_t *tab, const double *cdf, const uint64_t *ids, const double *x,
                int64_t n, double l1, int64_t L, int64_t K, uint64_t *out_fp, int32_t *phi_out,
                int64_t *hits_out);
+int or_bottom_k(const uint64_t *tab, const double *cdf, const uint64_t *ids, const double *x,
+                int64_t n, double l1, int64_t k, or_dart *out, int32_t *phi_out);
 int or_minhash_csr(const uint64_t *tab, const double *cdf, const int64_t *indptr,
                    const uint64_t *ids, const double *w, int64_t n, int64_t k, uint64_t *out,
                    int32_t *status, int32_t *phi, int64_t *hits, int nthreads);

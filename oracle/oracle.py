@@ -70,6 +70,9 @@ def lib():
         L.or_darts_flat.argtypes = [P, P, ctypes.c_int64, P, P, ctypes.c_int64, ctypes.c_double,
                                     ctypes.POINTER(ctypes.c_void_p)]
         L.or_free.argtypes = [P]
+        L.or_bottom_k.restype = ctypes.c_int
+        L.or_bottom_k.argtypes = [P, P, P, P, ctypes.c_int64, ctypes.c_double, ctypes.c_int64,
+                                  P, P]
         L.or_hash64_batch.argtypes = [P] * 8 + [ctypes.c_int64, P]
         del u64p
         _lib = L
@@ -138,6 +141,16 @@ class Oracle:
         arr = np.frombuffer(bytes(buf), dtype=DART_DTYPE).copy()
         lib().or_free(out)
         return 0, arr
+
+    def bottom_k(self, ids, weights, k: int):
+        """(status, phi, structured array of the k smallest darts) for one set."""
+        ids = np.ascontiguousarray(ids, dtype=np.uint64)
+        w = np.ascontiguousarray(weights, dtype=np.float64)
+        out = np.zeros(k, dtype=DART_DTYPE)
+        phi = ctypes.c_int32(0)
+        st = lib().or_bottom_k(_p(self.tables), _p(self.cdf), _p(ids), _p(w), ids.size,
+                               Oracle.pairwise_sum(w), int(k), _p(out), ctypes.byref(phi))
+        return int(st), int(phi.value), out
 
     # -- batch sketches --------------------------------------------------------
     def minhash_csr(self, indptr, ids, weights, k: int, nthreads: int | None = None):

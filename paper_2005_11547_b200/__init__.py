@@ -11,6 +11,16 @@ from .constants import ValidationError, minhash_density
 from . import shard, workloads
 from .api import (
     DSK_STATUS_TIE,
+    BottomKBatch,
+    BottomKFingerprints,
+    BottomKSketch,
+    bottom_k,
+    bottom_k_batch,
+    dump_sketch,
+    dump_sketches,
+    iter_sketches,
+    l1_batch,
+    load_sketch,
     Dart,
     DartBatch,
     DartHasher,
@@ -38,4 +48,6 @@ __all__ = [
     "HashFamily", "LshBatch", "LshParams", "MinhashBatch", "MinHashSketch", "OneBitSketch",
     "WeightedSet", "as_u64", "dart_minhash", "darts_batch", "lsh_batch", "lsh_key",
     "make_weighted_set", "minhash_batch", "one_bit", "raise_for_status", "weight_class",
+    "BottomKBatch", "BottomKFingerprints", "BottomKSketch", "bottom_k", "bottom_k_batch",
+    "dump_sketch", "dump_sketches", "iter_sketches", "l1_batch", "load_sketch",
 ]

@@ -19,7 +19,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_PATH = os.environ.get("DSK_LIB_PATH") or os.path.join(PKG, "libdsk_b200.so")
 HEADER = os.path.join(REPO, "include", "dsk_b200.h")
 SOURCES = ["dsk_kernels.cu", "dsk_device.cuh", "dsk_engine.cuh", "dsk_lsh_kernel.cuh",
-           "dsk_lsh_host.cuh"]
+           "dsk_lsh_host.cuh", "dsk_extra.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -91,6 +91,8 @@ SIGNATURES = [
     ("dsk_mix64", ctypes.c_int, [_P, _P, _I64, _I32, _P, _P]),
     ("dsk_pack_onebit", ctypes.c_int, [_P, _I64, _I32, _P, _P]),
     ("dsk_hash_peak", ctypes.c_int, [_P, _I64, _P, ctypes.POINTER(_I64), _P]),
+    ("dsk_l1_csr", ctypes.c_int, [_P, _P, _I64, _P, _P]),
+    ("dsk_dsk1_records", ctypes.c_int, [_I32, _I32, ctypes.c_uint64, _P, _I64, _P, _P]),
     ("dsk_last_error", ctypes.c_char_p, []),
 ]
 

@@ -566,6 +566,229 @@ def _resolve_minhash_ties(res: MinhashBatch, p, i, w, k, hashes, dev) -> None:
     res.status[tied] = res.status[tied] & 0xFF
 
 
+# ------------------------------------------------------------- bottom-k
+
+
+def l1_batch(indptr, weights, *, device=None) -> torch.Tensor:
+    """float(np.sum(weights)) per CSR row (ref/core.py:44), on the GPU."""
+    dev = _device(device)
+    p = _to_dev(indptr, torch.int64, dev)
+    w = _to_dev(weights, torch.float64, dev)
+    out = torch.empty(p.numel() - 1, dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().dsk_l1_csr(_ptr(p), _ptr(w), out.numel(), _ptr(out),
+                                          _stream_ptr(dev)), "dsk_l1_csr")
+    return out
+
+
+def _gather_rows(p: torch.Tensor, i: torch.Tensor, w: torch.Tensor, rows: torch.Tensor):
+    """Sub-CSR of the given rows, built on the device."""
+    lengths = p[rows + 1] - p[rows]
+    sub_p = torch.zeros(rows.numel() + 1, dtype=torch.int64, device=p.device)
+    torch.cumsum(lengths, 0, out=sub_p[1:])
+    total = int(sub_p[-1].item())
+    start = torch.repeat_interleave(p[rows], lengths, output_size=total)
+    base = torch.repeat_interleave(sub_p[:-1], lengths, output_size=total)
+    take = start + (torch.arange(total, device=p.device) - base)
+    return sub_p, i[take], w[take]
+
+
+def _lexsort_dev(keys):
+    """np.lexsort on the device: stable sorts, least significant key first."""
+    order = torch.arange(keys[0].numel(), device=keys[0].device)
+    for key in keys:
+        order = order[torch.sort(key[order], stable=True).indices]
+    return order
+
+
+@dataclass
+class BottomKBatch:
+    columns: dict                 # name -> tensor [n, k] (DartBatch columns, rank order)
+    status: torch.Tensor          # int32 [n]
+    phi: torch.Tensor             # int32 [n]
+
+
+def bottom_k_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, device=None,
+                   check: bool = True) -> BottomKBatch:
+    """bottom_k for every CSR row (ref/sketching.py:146-156): density t = k;
+    at the first phi step with >= k darts, the k smallest by (rank, index)."""
+    k = int(k)
+    if k < 1:
+        raise ValidationError(f"k must be positive, got {k}")
+    dev = _device(device)
+    p, i, w = _csr_to_dev(indptr, ids, weights, dev)
+    n = p.numel() - 1
+    l1 = l1_batch(p, w, device=dev)
+    cols = {name: torch.zeros((n, k), dtype=dt, device=dev) for name, dt in DART_COLUMNS}
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    phis = torch.zeros(n, dtype=torch.int32, device=dev)
+    empty = (p[1:] - p[:-1]) == 0
+    status[empty] = DSK_EMPTY
+    pending = torch.nonzero(~empty).flatten()
+    flip = torch.tensor(-(2**63), dtype=torch.int64, device=dev)
+    for phi in range(1, 65):  # ref/sketching.py:150
+        if pending.numel() == 0:
+            break
+        sp, si, sw = _gather_rows(p, i, w, pending)
+        limits = float(phi) / l1[pending]
+        offsets, st, dc = darts_batch(sp, si, sw, k, limits, hashes, device=dev)
+        bad = st != 0
+        if bool(bad.any()):
+            status[pending[bad]] = st[bad]
+        counts = offsets[1:] - offsets[:-1]
+        done = (counts >= k) & ~bad
+        if bool(done.any()):
+            owner = torch.repeat_interleave(torch.arange(pending.numel(), device=dev), counts)
+            sel_dart = done[owner]
+            idx = torch.nonzero(sel_dart).flatten()
+            o = owner[idx]
+            keys = [dc["j"][idx].to(torch.int64), dc["r"][idx].to(torch.int64) & 0xFFFFFFFF,
+                    dc["w"][idx].to(torch.int64) & 0xFFFFFFFF, dc["rho"][idx].to(torch.int64),
+                    dc["nu"][idx].to(torch.int64), dc["element"][idx] ^ flip, dc["rank"][idx], o]
+            order = idx[_lexsort_dev(keys)]
+            oo = owner[order]
+            first = torch.searchsorted(oo, oo, right=False)
+            pos = torch.arange(order.numel(), device=dev) - first
+            keep = pos < k
+            rows_out = pending[oo[keep]]
+            for name, _ in DART_COLUMNS:
+                cols[name][rows_out, pos[keep]] = dc[name][order[keep]]
+            phis[pending[done]] = phi
+        pending = pending[~done & ~bad]
+    if pending.numel():
+        status[pending] = DSK_NOCONV
+    res = BottomKBatch(cols, status, phis)
+    if check:
+        raise_for_status(status)
+    return res
+
+
+@dataclass(eq=False)
+class BottomKSketch:
+    """The k smallest-rank darts hitting a set, ascending (ref/sketching.py:40-53)."""
+
+    darts: list
+    k: int
+    seed: int
+
+    @property
+    def fingerprints(self) -> np.ndarray:
+        return np.asarray([d.fingerprint for d in self.darts], dtype=np.uint64)
+
+    def __eq__(self, other):
+        return (isinstance(other, BottomKSketch) and self.k == other.k
+                and self.seed == other.seed and self.darts == other.darts)
+
+    def __len__(self) -> int:
+        return self.k
+
+
+@dataclass(frozen=True)
+class BottomKFingerprints:
+    """Deserialized bottom-k record (ref/sketching.py:71-77)."""
+
+    values: np.ndarray = dataclasses.field(compare=False)
+    k: int = 0
+    seed: int = 0
+
+
+def bottom_k(x: WeightedSet, k: int, hashes: HashFamily) -> BottomKSketch:
+    """The first k darts hitting x, in ascending rank order (ref/sketching.py:146-156)."""
+    if x.is_empty():
+        raise ValidationError("cannot sketch an empty set")
+    if k < 1:
+        raise ValidationError(f"k must be positive, got {k}")
+    res = bottom_k_batch(*_single_csr(x), k, hashes)
+    h = {name: v[0].cpu().numpy() for name, v in res.columns.items()}
+    batch = DartBatch(h["element"].view(np.uint64), h["nu"].view(np.uint16),
+                      h["rho"].view(np.uint16), h["w"].view(np.uint32), h["r"].view(np.uint32),
+                      h["j"].view(np.uint16), h["weight"], h["rank"],
+                      h["fingerprint"].view(np.uint64))
+    return BottomKSketch(batch.to_darts(), k, hashes.seed)
+
+
+# ---------------------------------------------------------- DSK1 records
+
+SKETCH_MAGIC = b"DSK1"
+SKETCH_VERSION = 1
+KIND_MINHASH, KIND_ONEBIT, KIND_BOTTOMK = 1, 2, 3
+_HEADER_BYTES = 20  # struct "<4sBBHIQ", ref/sketching.py:221
+
+
+def dump_sketches(payload: torch.Tensor, kind: int, k: int, seed: int) -> bytes:
+    """DSK1 records for a batch, byte-identical to b"".join(dump_sketch(s) ...)
+    (ref/sketching.py:224-231), written on the GPU.
+
+    payload: device int64 tensor [n, k] of uint64 values (minhash, bottom-k
+    fingerprints) or [n, ceil(k/64)] packed one-bit words (kind 2)."""
+    dev = payload.device
+    n = payload.shape[0]
+    pbytes = (k + 7) // 8 if kind == KIND_ONEBIT else 8 * k
+    out = torch.empty(n * (_HEADER_BYTES + pbytes), dtype=torch.uint8, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().dsk_dsk1_records(int(kind), int(k), int(seed) & (2**64 - 1),
+                                                _ptr(payload.contiguous()), n, _ptr(out),
+                                                _stream_ptr(dev)), "dsk_dsk1_records")
+    return out.cpu().numpy().tobytes()
+
+
+def dump_sketch(sketch) -> bytes:
+    """Serialize one sketch (ref/sketching.py:224-231)."""
+    dev = _device(None)
+    if isinstance(sketch, MinHashSketch):
+        v = _to_dev(np.asarray(sketch.values, dtype=np.uint64), torch.int64, dev).view(1, -1)
+        return dump_sketches(v, KIND_MINHASH, sketch.k, sketch.seed)
+    if isinstance(sketch, OneBitSketch):
+        bits = np.asarray(sketch.bits, dtype=np.uint8)
+        words = (sketch.k + 63) // 64
+        packed = np.zeros(words * 8, dtype=np.uint8)
+        pb = np.packbits(bits, bitorder="little")
+        packed[:pb.size] = pb
+        v = _to_dev(packed.view("<u8"), torch.int64, dev).view(1, -1)
+        return dump_sketches(v, KIND_ONEBIT, sketch.k, sketch.seed)
+    if isinstance(sketch, (BottomKSketch, BottomKFingerprints)):
+        vals = sketch.fingerprints if isinstance(sketch, BottomKSketch) else sketch.values
+        v = _to_dev(np.asarray(vals, dtype=np.uint64), torch.int64, dev).view(1, -1)
+        return dump_sketches(v, KIND_BOTTOMK, sketch.k, sketch.seed)
+    raise ValidationError(f"cannot serialize object of type {type(sketch).__name__}")
+
+
+def iter_sketches(data: bytes):
+    """Parse concatenated DSK1 records (ref/sketching.py:234-281)."""
+    import struct
+    hdr = struct.Struct("<4sBBHIQ")
+    off = 0
+    while off < len(data):
+        if len(data) - off < hdr.size:
+            raise ValidationError("truncated sketch record")
+        magic, version, kind, _, k, seed = hdr.unpack_from(data, off)
+        if magic != SKETCH_MAGIC:
+            raise ValidationError(f"bad sketch magic {magic!r}")
+        if version != SKETCH_VERSION:
+            raise ValidationError(f"unsupported sketch version {version}")
+        off += hdr.size
+        size = (k + 7) // 8 if kind == KIND_ONEBIT else 8 * k
+        if len(data) - off < size:
+            raise ValidationError("truncated sketch payload")
+        payload = data[off:off + size]
+        off += size
+        if kind == KIND_MINHASH:
+            yield MinHashSketch(np.frombuffer(payload, dtype="<u8").astype(np.uint64), k, seed)
+        elif kind == KIND_ONEBIT:
+            bits = np.unpackbits(np.frombuffer(payload, dtype=np.uint8), count=k,
+                                 bitorder="little")
+            yield OneBitSketch(bits, k, seed)
+        elif kind == KIND_BOTTOMK:
+            yield BottomKFingerprints(np.frombuffer(payload, dtype="<u8").astype(np.uint64), k,
+                                      seed)
+        else:
+            raise ValidationError(f"unknown sketch kind {kind}")
+
+
+def load_sketch(data: bytes, offset: int = 0):
+    return next(iter_sketches(data[offset:]))
+
+
 # --------------------------------------------------------- single-set API
 
 
@@ -670,6 +893,8 @@ __all__ = [
     "MinHashSketch", "OneBitSketch", "LshParams", "weight_class", "minhash_density",
     "dart_minhash", "one_bit", "lsh_key", "minhash_batch", "lsh_batch", "darts_batch",
     "MinhashBatch", "LshBatch", "ValidationError", "raise_for_status", "as_u64",
-    "DSK_STATUS_TIE",
+    "DSK_STATUS_TIE", "l1_batch", "bottom_k_batch", "BottomKBatch", "BottomKSketch",
+    "BottomKFingerprints", "bottom_k", "dump_sketches", "dump_sketch", "iter_sketches",
+    "load_sketch",
 ]
 _ = dataclasses

@@ -1,0 +1,76 @@
+// dsk_extra.cuh -- small batch kernels around the hot path (included at the
+// end of dsk_kernels.cu):
+//   dsk_l1_csr        float(np.sum(weights)) per set (ref/core.py:44), the
+//                     rank-limit denominator of every phi step
+//   dsk_dsk1_records  DSK1 sketch records (ref/sketching.py:210-231) for a
+//                     batch, byte-identical to concatenated dump_sketch()
+
+__global__ void l1_kernel(const int64_t *indptr, const double *w, int64_t n, double *out) {
+  __shared__ double scratch[8][256];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t s = (int64_t)blockIdx.x * 8 + warp; s < n; s += (int64_t)gridDim.x * 8) {
+    const int64_t lo = indptr[s], nnz = indptr[s + 1] - lo;
+    double l1 = warp_np_sum(w + lo, nnz, scratch[warp], lane, 0);
+    if (lane == 0) out[s] = l1;
+  }
+}
+
+extern "C" int dsk_l1_csr(const int64_t *indptr, const double *weights, int64_t n, double *out,
+                          void *stream) {
+  if (!indptr || !weights || !out || n < 0) return set_err(DSK_EARG, "bad argument");
+  if (n == 0) return DSK_OK;
+  int grid = (int)((n + 7) / 8);
+  if (grid > 148 * 16) grid = 148 * 16;
+  l1_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(indptr, weights, n, out);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}
+
+// header <4sBBHIQ: "DSK1", version 1, kind, reserved 0, k, seed (ref/sketching.py:221)
+__global__ void dsk1_kernel(int kind, uint32_t k, uint64_t seed, const uint64_t *payload,
+                            int64_t words_per_set, int64_t payload_bytes, int64_t n,
+                            uint8_t *out) {
+  const int64_t rec = 20 + payload_bytes;
+  const int64_t total = n * rec;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t s = i / rec, o = i - s * rec;
+    uint8_t b;
+    if (o < 4) {
+      b = (uint8_t)("DSK1"[o]);
+    } else if (o == 4) {
+      b = 1;  // SKETCH_VERSION
+    } else if (o == 5) {
+      b = (uint8_t)kind;
+    } else if (o < 8) {
+      b = 0;  // reserved
+    } else if (o < 12) {
+      b = (uint8_t)(k >> (8 * (o - 8)));
+    } else if (o < 20) {
+      b = (uint8_t)(seed >> (8 * (o - 12)));
+    } else {
+      const int64_t p = o - 20;  // little-endian payload byte p of set s
+      b = (uint8_t)(payload[s * words_per_set + (p >> 3)] >> (8 * (p & 7)));
+    }
+    out[i] = b;
+  }
+}
+
+// kind 1 (minhash) and 3 (bottom-k): payload = k uint64 values per set;
+// kind 2 (one-bit): payload = ceil(k/8) bytes of the packed words
+// (np.packbits(bits, bitorder="little"), ref/sketching.py:229).
+extern "C" int dsk_dsk1_records(int32_t kind, int32_t k, uint64_t seed, const uint64_t *payload,
+                                int64_t n, uint8_t *out, void *stream) {
+  if (!payload || !out || n < 0 || k < 1 || kind < 1 || kind > 3)
+    return set_err(DSK_EARG, "bad argument");
+  if (n == 0) return DSK_OK;
+  const int64_t words = kind == 2 ? (k + 63) / 64 : k;
+  const int64_t pbytes = kind == 2 ? (k + 7) / 8 : 8 * (int64_t)k;
+  int64_t total = n * (20 + pbytes);
+  int grid = (int)((total + 255) / 256);
+  if (grid > 148 * 32) grid = 148 * 32;
+  dsk1_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(kind, (uint32_t)k, seed, payload, words,
+                                                      pbytes, n, out);
+  CUDA_TRY(cudaGetLastError());
+  return DSK_OK;
+}

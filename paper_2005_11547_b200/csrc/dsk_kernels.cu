@@ -959,3 +959,4 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
 }
 
 #include "dsk_lsh_host.cuh"
+#include "dsk_extra.cuh"

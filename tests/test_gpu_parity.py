@@ -411,3 +411,73 @@ def test_tie_resolution_path():
     assert np.array_equal(as_u64(res.values), good)
     assert np.array_equal(as_u64(res.bits), good_bits)
     assert (res.status.cpu().numpy() == 0).all()
+
+
+# ------------------------------------------------- bottom-k and DSK1 (next rows)
+
+
+def test_l1_batch_matches_numpy():
+    from paper_2005_11547_b200 import l1_batch
+    rng = np.random.default_rng(4)
+    sizes = [0, 1, 5, 8, 127, 128, 129, 1000, 1024, 4097, 16384, 16385, 40000]
+    lens = np.array(sizes, dtype=np.int64)
+    indptr = np.zeros(lens.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    w = rng.lognormal(0.0, 3.0, int(indptr[-1]))
+    got = l1_batch(indptr, w).cpu().numpy()
+    exp = np.array([float(np.sum(w[indptr[s]:indptr[s + 1]])) for s in range(lens.size)])
+    assert np.array_equal(got, exp)
+
+
+def test_bottom_k_golden():
+    from paper_2005_11547_b200 import bottom_k_batch
+    g = golden("bottomk_dsk1.npz")
+    f = fam(int(g["seed"]))
+    n = g["indptr"].size - 1
+    for k in (1, 3, 17, 64):
+        res = bottom_k_batch(g["indptr"], g["ids"], g["w"], k, f)
+        exp = g[f"bottomk_k{k}"].reshape(n, k)
+        cols = {name: v.cpu().numpy() for name, v in res.columns.items()}
+        for name in exp.dtype.names:
+            got = cols[name]
+            if name in ("element", "fingerprint"):
+                got = got.view(np.uint64)
+            elif name in ("nu", "rho", "j"):
+                got = got.view(np.uint16)
+            elif name in ("w", "r"):
+                got = got.view(np.uint32)
+            assert np.array_equal(got, exp[name]), (k, name)
+
+
+def test_bottom_k_single_set_api_and_oracle():
+    from paper_2005_11547_b200 import bottom_k
+    f = fam(0xBEEF)
+    x = make_weighted_set([(1, 0.5), (2, 0.25), (3, 1.25)])
+    sk = bottom_k(x, 12, f)
+    # tests/test_sketching.py:112-117: prefix of the (rank, index)-ordered darts
+    universe = DartHasher(12, f).darts(x, 64.0)
+    assert sk.darts == sorted(universe, key=lambda d: (d.rank, d.index))[:12]
+    indptr, ids, w = workloads.generate("cfg3", n=40)
+    orc = Oracle(2)
+    from paper_2005_11547_b200 import bottom_k_batch
+    res = bottom_k_batch(indptr, ids, w, 64, fam(2))
+    fp = as_u64(res.columns["fingerprint"])
+    for s in range(40):
+        st, _, od = orc.bottom_k(ids[indptr[s]:indptr[s + 1]], w[indptr[s]:indptr[s + 1]], 64)
+        assert st == 0 and np.array_equal(fp[s], od["fingerprint"])
+
+
+def test_dsk1_records_byte_identical():
+    from paper_2005_11547_b200 import (BottomKFingerprints, MinHashSketch, bottom_k_batch,
+                                       dump_sketches, iter_sketches)
+    g = golden("bottomk_dsk1.npz")
+    f = fam(int(g["seed"]))
+    res = minhash_batch(g["indptr"], g["ids"], g["w"], 100, f, bits=True)
+    assert dump_sketches(res.values, 1, 100, f.seed) == g["dsk1_minhash"].tobytes()
+    assert dump_sketches(res.bits, 2, 100, f.seed) == g["dsk1_onebit"].tobytes()
+    bk = bottom_k_batch(g["indptr"], g["ids"], g["w"], 17, f)
+    assert dump_sketches(bk.columns["fingerprint"], 3, 17, f.seed) == g["dsk1_bottomk"].tobytes()
+    recs = list(iter_sketches(g["dsk1_minhash"].tobytes()))
+    assert isinstance(recs[0], MinHashSketch)
+    assert np.array_equal(np.stack([r.values for r in recs]), as_u64(res.values))
+    assert isinstance(list(iter_sketches(g["dsk1_bottomk"].tobytes()))[0], BottomKFingerprints)

@@ -172,3 +172,19 @@ def test_lsh_11_equals_minhash_1():
     vals, _, _, _ = orc.minhash_csr(g["indptr"], g["ids"], g["w"], 1)
     assert np.array_equal(fps[:, 0, 0], vals[:, 0])
     assert math.isfinite(float(vals.size))
+
+
+def test_bottom_k_matches_reference():
+    # ref/sketching.py:146-156 outputs, tuple for tuple
+    g = golden("bottomk_dsk1.npz")
+    orc = Oracle(int(g["seed"]))
+    indptr = g["indptr"]
+    for k in (1, 3, 17, 64):
+        exp = g[f"bottomk_k{k}"]
+        for s in range(indptr.size - 1):
+            st, _, darts = orc.bottom_k(g["ids"][indptr[s]:indptr[s + 1]],
+                                        g["w"][indptr[s]:indptr[s + 1]], k)
+            assert st == 0
+            row = exp[s * k:(s + 1) * k]
+            for name in row.dtype.names:
+                assert np.array_equal(darts[name], row[name]), (k, s, name)
