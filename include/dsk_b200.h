@@ -128,11 +128,13 @@ int dsk_mix64(dsk_ctx *ctx, const uint64_t *values, int64_t nseq, int32_t len, u
 int dsk_pack_onebit(const uint64_t *values, int64_t n, int32_t k, uint64_t *out_bits,
                     void *stream);
 
-/* K0 hash-rate microbenchmark: n_per_thread dependent-free hashes per thread
- * (one table lookup + splitmix64 each, the minimum a hoisted dart hash
- * costs) over a full-device grid; xor of results into sink[0]. */
-int dsk_hash_peak(dsk_ctx *ctx, int64_t n_per_thread, uint64_t *sink, int64_t *hashes_done,
-                  void *stream);
+/* K0 hash-rate microbenchmark over a full-device grid (4 chains per thread,
+ * n_per_thread hashes per chain; xor of results into sink[0]).
+ * mode 0: a full hash evaluation as the reference defines it -- 22 table
+ * lookups + splitmix64 (ref/randomness.py:121-131): the ALU roofline
+ * denominator.  mode 1: one lookup + splitmix64, the cheapest hoisted hash. */
+int dsk_hash_peak(dsk_ctx *ctx, int32_t mode, int64_t n_per_thread, uint64_t *sink,
+                  int64_t *hashes_done, void *stream);
 
 /* float(np.sum(weights)) of every set (ref/core.py:44, numpy pairwise order):
  * the denominator of each phi step's rank limit phi / ||x||_1. */
