@@ -149,6 +149,14 @@ int dsk_l1_csr(const int64_t *indptr, const double *weights, int64_t n, double *
 int dsk_dsk1_records(int32_t kind, int32_t k, uint64_t seed, const uint64_t *payload, int64_t n,
                      uint8_t *out, void *stream);
 
+/* exact_jaccard (ref/core.py:103-120) for npairs (row pa[t] of set batch A,
+ * row pb[t] of set batch B); rows must hold ids sorted ascending.  Sums run
+ * in ascending id order like the reference, so results are bit-identical. */
+int dsk_exact_jaccard(const int64_t *a_ptr, const uint64_t *a_ids, const double *a_w,
+                      const int64_t *b_ptr, const uint64_t *b_ids, const double *b_w,
+                      const int64_t *pa, const int64_t *pb, int64_t npairs, double *out,
+                      void *stream);
+
 const char *dsk_last_error(void);
 
 #ifdef __cplusplus

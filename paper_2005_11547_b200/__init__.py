@@ -8,7 +8,7 @@ DESIGN.md for the boundary and INTEGRATION.md for the ctypes binding.
 """
 
 from .constants import ValidationError, minhash_density
-from . import shard, workloads
+from . import io, shard, workloads
 from .api import (
     DSK_STATUS_TIE,
     BottomKBatch,
@@ -51,3 +51,7 @@ __all__ = [
     "BottomKBatch", "BottomKFingerprints", "BottomKSketch", "bottom_k", "bottom_k_batch",
     "dump_sketch", "dump_sketches", "iter_sketches", "l1_batch", "load_sketch",
 ]
+
+from .lsh_index import LshIndex, probe_classes  # noqa: E402
+
+__all__ += ["LshIndex", "probe_classes"]

@@ -93,6 +93,7 @@ SIGNATURES = [
     ("dsk_hash_peak", ctypes.c_int, [_P, _I32, _I64, _P, ctypes.POINTER(_I64), _P]),
     ("dsk_l1_csr", ctypes.c_int, [_P, _P, _I64, _P, _P]),
     ("dsk_dsk1_records", ctypes.c_int, [_I32, _I32, ctypes.c_uint64, _P, _I64, _P, _P]),
+    ("dsk_exact_jaccard", ctypes.c_int, [_P, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P]),
     ("dsk_last_error", ctypes.c_char_p, []),
 ]
 

@@ -481,3 +481,57 @@ def test_dsk1_records_byte_identical():
     assert isinstance(recs[0], MinHashSketch)
     assert np.array_equal(np.stack([r.values for r in recs]), as_u64(res.values))
     assert isinstance(list(iter_sketches(g["dsk1_bottomk"].tobytes()))[0], BottomKFingerprints)
+
+
+# ------------------------------------------------------- LshIndex (next row)
+
+
+def _sets_from_csr(indptr, ids, w):
+    return [WeightedSet.from_arrays(ids[indptr[s]:indptr[s + 1]], w[indptr[s]:indptr[s + 1]])
+            for s in range(indptr.size - 1)]
+
+
+def test_lsh_index_matches_reference():
+    from paper_2005_11547_b200 import LshIndex
+    g = golden("lsh_index.npz")
+    f = fam(int(g["seed"]))
+    params = LshParams(int(g["L"]), int(g["K"]), float(g["j1"]))
+    idx = LshIndex(params, f, debug=True)
+    pts = _sets_from_csr(g["p_indptr"], g["p_ids"], g["p_w"])
+    idx.insert_many(list(range(50)), pts[:50])
+    for i in range(50, len(pts)):  # single inserts interleaved with a query
+        idx.insert(i, pts[i])
+    assert len(idx) == len(pts)
+    for i in range(len(pts)):
+        c, keys = idx._debug_keys[i]
+        assert c == g["classes"][i]
+        assert np.array_equal(keys, g["keys"][i])
+    qs = _sets_from_csr(g["q_indptr"], g["q_ids"], g["q_w"])
+    results = idx.query_many(qs)
+    ptr = g["res_ptr"]
+    for qi, r in enumerate(results):
+        exp = list(zip(g["res_pid"][ptr[qi]:ptr[qi + 1]].tolist(),
+                       g["res_score"][ptr[qi]:ptr[qi + 1]].tolist()))
+        assert r == exp, qi
+    assert idx.query(qs[3]) == results[3]
+
+
+def test_lsh_index_semantics():
+    from paper_2005_11547_b200 import LshIndex
+    f = fam(0x1E0)
+    idx = LshIndex(LshParams(L=4, K=2), f)
+    assert idx.query(make_weighted_set([(1, 1.0)])) == []
+    rng = np.random.default_rng(4)
+    xs = [WeightedSet.from_arrays(rng.choice(10**6, 12, replace=False).astype(np.uint64),
+                                  rng.random(12) * 2.0 ** rng.uniform(-3, 3) + 1e-3)
+          for _ in range(20)]
+    idx.insert_many(range(20), xs)
+    for i, x in enumerate(xs):  # tests/test_annindex.py:94-103
+        r = idx.query(x)
+        assert r and r[0] == (i, 1.0)
+    with pytest.raises(ValidationError):
+        idx.insert(3, xs[0])
+    with pytest.raises(ValidationError):
+        idx.insert(99, make_weighted_set([]))
+    with pytest.raises(ValidationError):
+        idx.query(make_weighted_set([]))
