@@ -34,6 +34,15 @@
 #pragma once
 #include "dsk_device.cuh"
 
+// DSK_DEBUG builds check the ring-capacity and indexing invariants the
+// scheduler relies on (compute-sanitizer is unavailable on this pool).
+#ifdef DSK_DEBUG
+#include <assert.h>
+#define DSK_CHECK(c) assert(c)
+#else
+#define DSK_CHECK(c) ((void)0)
+#endif
+
 namespace dsk {
 
 // build-time tunables (profiles/sweep.sh builds variants)
@@ -261,6 +270,7 @@ struct Engine {
       Q.ht[idx] = make_ulonglong2(fpkey, (unsigned long long)__double_as_longlong(rank));
     }
     ht_cnt += __popc(b);
+    DSK_CHECK(ht_cnt <= kQ);
   }
 
   __device__ __forceinline__ void push_area(bool valid, uint64_t pa, double x, uint32_t w,
@@ -272,6 +282,7 @@ struct Engine {
       Q.arB[idx] = make_uint4(w, r, meta, elem);
     }
     ar_cnt += __popc(b);
+    DSK_CHECK(ar_cnt <= kQR);
   }
 
   __device__ __forceinline__ void push_region(bool valid, uint64_t pr, double x, uint32_t whi,
@@ -283,6 +294,7 @@ struct Engine {
       Q.rgB[idx] = make_uint4(whi, rlo, rhi, meta);
     }
     rg_cnt += __popc(b);
+    DSK_CHECK(rg_cnt <= kQR);
   }
 
   // ----------------------------------------------------------------- hits
@@ -313,6 +325,7 @@ struct Engine {
   // ---------------------------------------------------------------- darts
   // darts [ar_cur, ar_cur + 64) of the head areas (ref/darthash.py:264-292)
   __device__ void areas_step() {
+    DSK_CHECK(ht_cnt < kStep);
     const int mp = ar_cnt < 32 ? ar_cnt : 32;
     uint32_t c = lane < mp ? (Q.arB[ringR(ar_head + lane)].z >> 16) & 0xff : 0;
     HeadScan hs = head_scan(c, mp, lane);
@@ -403,6 +416,7 @@ struct Engine {
   // (ref/darthash.py:248-262), with the Poisson(1) count of each
   // (ref/randomness.py:145-147, :209-211: j = 0, stream 3)
   __device__ void regions_step() {
+    DSK_CHECK(ar_cnt < 32);
     const int mp = rg_cnt < 32 ? rg_cnt : 32;
     uint32_t c = 0;
     if (lane < mp) {
@@ -542,6 +556,7 @@ struct Engine {
   }
 
   __device__ void direct_step() {
+    DSK_CHECK(ar_cnt < 32);
     // refill idle walkers with the chunk's next runs
     bool idle = wk_a >= wk_end;
     unsigned idle_mask = __ballot_sync(DSK_FULL, idle);
@@ -607,6 +622,7 @@ struct Engine {
   // regions [el_cur, el_cur + 64) of the element chunk: the surviving
   // rectangle of each (nu, rho) (ref/darthash.py:180-225)
   __device__ void element_step() {
+    DSK_CHECK(rg_cnt < 32);
     const int rdp1 = P.RD + 1;
     const float inv_rdp1 = 1.0f / (float)rdp1;
     const float inv_rd = P.RD > 0 ? 1.0f / (float)P.RD : 0.0f;
@@ -648,6 +664,7 @@ struct Engine {
         int64_t r_hi, r_lo = 0;
         uint32_t flags = 0;
         if (use_table) {
+          DSK_CHECK(nu * rdp1 + rho < kRwin);
           uint4 rw = rwin[nu * rdp1 + rho];
           r_hi = (int64_t)rw.x - 1;
           if (rw.y & 0x80000000u) { r_lo = rw.y & 0x7fffffffu; flags |= kRgHasPrev >> 16; }

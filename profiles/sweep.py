@@ -15,6 +15,7 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
+    "debug": {"DSK_DEBUG": 1},
     "run4": {"DSK_RUN": 4},
     "w20run4": {"DSK_WARPS": 20, "DSK_RUN": 4},
     "w22run4": {"DSK_WARPS": 22, "DSK_RUN": 4},

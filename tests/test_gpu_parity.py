@@ -535,3 +535,54 @@ def test_lsh_index_semantics():
         idx.insert(99, make_weighted_set([]))
     with pytest.raises(ValidationError):
         idx.query(make_weighted_set([]))
+
+
+# ------------------------------------------- statistical laws (cheap re-checks)
+
+
+def _pair(rng, l0, J):
+    """x and a companion y with weighted Jaccard J (ref/bench.py:103-121 construction)."""
+    ids = rng.choice(2**40, l0, replace=False).astype(np.uint64)
+    e = -np.log1p(-rng.random(l0))
+    w = e / e.sum()
+    b = 2.0 * J / (1.0 + J)
+    fresh = np.uint64(2**41 + int(rng.integers(0, 2**20)))
+    y_ids = np.concatenate([ids, [fresh]])
+    y_w = np.concatenate([w * b, [(1.0 - b) * float(np.sum(w))]])
+    return (ids, w), (y_ids, y_w)
+
+
+def test_collision_rate_tracks_similarity():
+    # tests/test_sketching.py:65-76: per coordinate P[collision] = J
+    k, trials, J = 256, 200, 0.5
+    rng = np.random.default_rng(900)
+    rows = []
+    for _ in range(trials):
+        x, y = _pair(rng, 24, J)
+        rows += [x, y]
+    indptr = np.zeros(len(rows) + 1, dtype=np.int64)
+    np.cumsum([r[0].size for r in rows], out=indptr[1:])
+    ids = np.concatenate([r[0] for r in rows])
+    w = np.concatenate([r[1] for r in rows])
+    v = as_u64(minhash_batch(indptr, ids, w, k, fam(7000)).values)
+    est = (v[0::2] == v[1::2]).mean()
+    se = (J * (1 - J) / (k * trials)) ** 0.5
+    assert abs(est - J) <= 4 * se
+
+
+def test_dart_count_is_poisson():
+    # tests/test_darthash.py:85-96: mean dart count at phi = 1 is t
+    from paper_2005_11547_b200 import l1_batch
+    rng = np.random.default_rng(1312)
+    t, sets = 1000, 400
+    lens = np.full(sets, 32)
+    indptr = np.zeros(sets + 1, dtype=np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    ids = np.concatenate([rng.choice(2**40, 32, replace=False) for _ in range(sets)]).astype(np.uint64)
+    w = rng.random(indptr[-1]) + 1e-3
+    l1 = l1_batch(indptr, w).cpu().numpy()
+    offsets, status, _ = darts_batch(indptr, ids, w, t, 1.0 / l1, fam(11))
+    counts = np.diff(offsets.cpu().numpy())
+    assert (status.cpu().numpy() == 0).all()
+    assert abs(counts.mean() - t) <= 4 * (t / sets) ** 0.5
+    assert abs(counts.var() / t - 1.0) < 0.25
