@@ -83,6 +83,12 @@ __device__ __forceinline__ int64_t rank_window(double limit, int nu, int rho, do
 __device__ __forceinline__ int64_t weight_window(double x, double w0, double dnu, double tpow,
                                                  int rho) {
   if (rho == 0) return w0 <= x ? 0 : -1;  // wmax = 0: only candidate 0, w0 + 0*dnu == w0
+  if (rho == 1) {
+    // wmax = 1: the clamped base is 0 or 1, so the +-2 window covers both
+    // candidates and the result is the largest passing one (no estimate needed)
+    if (__dadd_rn(w0, dnu) <= x) return 1;
+    return w0 <= x ? 0 : -1;
+  }
   double wmax = __dadd_rn(pow2(rho), -1.0);  // float(2^rho - 1) as numpy compares it
   double capw = wmax < kCandClip ? wmax : kCandClip;
   double base = floor(__dmul_rn(__dadd_rn(x, -w0), tpow));

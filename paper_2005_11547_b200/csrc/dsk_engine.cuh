@@ -53,7 +53,7 @@ namespace dsk {
 #define DSK_RUN 4
 #endif
 #ifndef DSK_DIRECT
-#define DSK_DIRECT 1
+#define DSK_DIRECT 2  // 0: off, 1: only when the rank depth is 0, 2: always when tables fit
 #endif
 #ifndef DSK_REFILL
 #define DSK_REFILL 8
@@ -253,9 +253,8 @@ struct Engine {
         carry_f = __shfl_sync(DSK_FULL, fi, 31);
       }
       // row counts stay far below 2^31 for every legal step
-      // (sets with rank depth >= 1 have few areas per rho = 0 row: the region
-      // ring expands them more cheaply than short walker runs)
-      direct = DSK_DIRECT && P.RD == 0 && __all_sync(DSK_FULL, narrow) && carry_a < (1u << 30) &&
+      direct = DSK_DIRECT && (P.RD == 0 || DSK_DIRECT == 2) && __all_sync(DSK_FULL, narrow) &&
+               carry_a < (1u << 30) &&
                carry_f < (1u << 30);
     }
     __syncwarp();

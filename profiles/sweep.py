@@ -15,12 +15,11 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "debug": {"DSK_DEBUG": 1},
-    "run4": {"DSK_RUN": 4},
-    "w20run4": {"DSK_WARPS": 20, "DSK_RUN": 4},
-    "w22run4": {"DSK_WARPS": 22, "DSK_RUN": 4},
-    "w20run6": {"DSK_WARPS": 20, "DSK_RUN": 6},
-    "run4ref4": {"DSK_RUN": 4, "DSK_REFILL": 4},
+    "base": {},
+    "directall": {"DSK_DIRECT": 2},
+    "run2": {"DSK_RUN": 2},
+    "run3": {"DSK_RUN": 3},
+    "refill12": {"DSK_REFILL": 12},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
