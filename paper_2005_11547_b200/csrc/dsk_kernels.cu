@@ -874,7 +874,7 @@ extern "C" int dsk_hash_peak(dsk_ctx *c, int32_t mode, int64_t n_per_thread, uin
 // ------------------------------------------------------ host-buffer calls
 //
 // dsk_*_csr_host: the drop-in for a caller holding numpy arrays.  Rows are
-// cut into chunks of ~64 MB of input; chunk c is copied in, sketched and
+// cut into chunks of ~128 MB of input; chunk c is copied in, sketched and
 // copied out on stream c % 2, so the PCIe transfers of one chunk overlap the
 // kernel of the other.  Device staging is owned by the context and reused.
 
@@ -949,7 +949,9 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
   constexpr int kMaxChunks = 64;
   int64_t bounds[kMaxChunks + 1];
   int nch = 0;
-  plan_chunks(indptr, n, (size_t)64 << 20, bounds, kMaxChunks + 1, &nch);
+  size_t chunk_mb = 128;  // ~2 ms of PCIe per chunk: balances copy and kernel time
+  if (const char *e = getenv("DSK_CHUNK_MB")) chunk_mb = (size_t)atoi(e) > 0 ? (size_t)atoi(e) : 128;
+  plan_chunks(indptr, n, chunk_mb << 20, bounds, kMaxChunks + 1, &nch);
   CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, c->hs[0]));
   CUDA_TRY(cudaEventRecord(c->ev_in[0], c->hs[0]));
   CUDA_TRY(cudaStreamWaitEvent(c->hs[1], c->ev_in[0], 0));
