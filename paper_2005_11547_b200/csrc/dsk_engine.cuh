@@ -53,11 +53,15 @@ namespace dsk {
 #define DSK_RUN 4
 #endif
 #ifndef DSK_DIRECT
-#define DSK_DIRECT 2  // 0: off, 1: only when the rank depth is 0, 2: always when tables fit
+#define DSK_DIRECT 1  // 0: off, 1: only when the rank depth is 0, 2: always when tables fit
 #endif
 #ifndef DSK_REFILL
 #define DSK_REFILL 8
 #endif
+#ifndef DSK_FUSE
+#define DSK_FUSE 2  // dart 0 finished at area creation: 0 never, 1 direct walkers, 2 both paths
+#endif
+// (per sink: the LSH sink measured faster without the fusion, Sink::kFuse)
 
 constexpr int kILP = 1;      // children per lane per stage step (independent chains)
 constexpr int kStep = 32 * kILP;
@@ -99,7 +103,8 @@ struct WarpQueues {
 constexpr uint32_t kRgHasPrev = 1u << 16, kRgWide = 1u << 17, kRgNarrow = 1u << 18,
                    kRgWEdge = 1u << 19;  // the w_hi column can hold darts heavier than x
 // area meta: nu | rho << 8 | count << 16 | flags << 24
-constexpr uint32_t kArWb = 1u << 24, kArRb = 1u << 25, kArLb = 1u << 26;
+constexpr uint32_t kArWb = 1u << 24, kArRb = 1u << 25, kArLb = 1u << 26,
+                   kArJ1 = 1u << 27;  // dart 0 was evaluated when the area was made
 
 struct PassParams {
   const uint64_t *gtab;  // global 22x256 tables (rare wide-key bytes)
@@ -322,87 +327,89 @@ struct Engine {
   }
 
   // ---------------------------------------------------------------- darts
-  // darts [ar_cur, ar_cur + 64) of the head areas (ref/darthash.py:264-292)
+  // Dart j of an area with uniform u (U stream) already drawn: rank, the
+  // rank / weight tests (ref/darthash.py:264-292), and the hit (warp-collective).
+  __device__ __forceinline__ void finish_dart(bool valid, uint64_t pa, uint32_t meta, uint32_t w,
+                                              uint32_t r, double x, uint32_t j, double u,
+                                              uint32_t elem) {
+    const int nu = meta & 0xff, rho = (meta >> 8) & 0xff;
+    // rank = r0 + (r + u) * drho, ref/darthash.py:282 (separately rounded)
+    const double r0 = __dadd_rn(pow2(rho), -1.0);
+    const double rank = __dadd_rn(r0, __dmul_rn(__dadd_rn((double)r, u), pow2(rho - nu)));
+    bool hit = valid;
+    if (meta & kArRb) hit = hit && rank <= P.L_hi;  // interior rows pass by monotonicity
+    if (meta & kArLb) hit = hit && rank > P.L_lo;   // band: exclude darts seen before
+    const bool needv = hit && (kFull || (meta & kArWb));  // only the w_hi column can miss
+    double weight = 0.0;
+    if (__any_sync(DSK_FULL, needv)) {
+      double v = u53(finalize(pa ^ T.js[j][kStreamV - 1]));
+      double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
+      // weight = w0 + (w + v) * dnu, ref/darthash.py:281
+      weight = __dadd_rn(T.w0[nu], __dmul_rn(__dadd_rn((double)w, v), dnu));
+      if (needv && (meta & kArWb)) hit = weight <= x;  // inclusive, ref/darthash.py:284
+    }
+    if (kFull) {  // materialising sink: every hit with its full index tuple
+      if (hit) {
+        DartRow d;
+        d.elem = elem;
+        d.nu = nu;
+        d.rho = rho;
+        d.w = w;
+        d.r = r;
+        d.j = j;
+        d.weight = weight;
+        d.rank = rank;
+        d.fp = finalize(pa ^ T.js[j][kStreamFp - 1]);
+        sink.row(d);
+        n_hits++;
+      }
+    } else {
+      push_hit(hit, rank, pa ^ T.js[j][kStreamFp - 1]);
+    }
+  }
+
+  // Area (w, r) with key prefix pa: its Poisson(1) count (ref/randomness.py:
+  // 145-147, j = 0, stream 3) and, from the same key, the U draw of dart 0
+  // (an independent hash chain); dart 0 is finished here and only areas with
+  // further darts enter the area ring (count - 1 darts, starting at j = 1).
+  template <bool kFuse>
+  __device__ __forceinline__ void emit_area(bool valid, uint64_t pa, double x, uint32_t w,
+                                            uint32_t r, uint32_t meta, bool lb, uint32_t elem) {
+    if (!kFuse) {
+      const uint32_t k = poisson_count(finalize(pa ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
+      const uint32_t cnt = valid ? k : 0;
+      if (!lb) n_darts += cnt;
+      push_area(cnt > 0, pa, x, w, r, meta | (cnt << 16), elem);
+      return;
+    }
+    const uint64_t hp = finalize(pa ^ T.js[0][kStreamPoisson - 1]);
+    const uint64_t hu = finalize(pa ^ T.js[0][kStreamU - 1]);
+    const uint32_t k = poisson_count(hp >> 11, P, T);
+    const uint32_t cnt = valid ? k : 0;
+    if (!lb) n_darts += cnt;
+    finish_dart(cnt > 0, pa, meta, w, r, x, 0, u53(hu), elem);
+    push_area(cnt > 1, pa, x, w, r, meta | ((cnt - 1) << 16) | kArJ1, elem);
+  }
+
+  // darts [ar_cur, ar_cur + 32) of the head areas, j >= 1 (dart 0 was
+  // finished when the area was made)
   __device__ void areas_step() {
     DSK_CHECK(ht_cnt < kStep);
     const int mp = ar_cnt < 32 ? ar_cnt : 32;
     uint32_t c = lane < mp ? (Q.arB[ringR(ar_head + lane)].z >> 16) & 0xff : 0;
     HeadScan hs = head_scan(c, mp, lane);
     const uint32_t lo = ar_cur, hi = lo + kStep < hs.total ? lo + kStep : hs.total;
-    bool valid[kILP], hit[kILP], needv[kILP];
-    uint32_t j[kILP], meta[kILP];
-    int ai[kILP];
-    uint64_t pa[kILP];
-    double rank[kILP], x[kILP];
-    uint4 B[kILP];
-#pragma unroll
-    for (int q = 0; q < kILP; q++) {
-      uint32_t pos = lo + lane + 32 * q;
-      valid[q] = pos < hi;
-      int src = warp_owner(hs.excl, pos);
-      j[q] = (pos - __shfl_sync(DSK_FULL, hs.excl, src)) & (kJs - 1);
-      ai[q] = ringR(ar_head + src);
-    }
-#pragma unroll
-    for (int q = 0; q < kILP; q++) {
-      ulonglong2 A = Q.arA[ai[q]];
-      B[q] = Q.arB[ai[q]];
-      pa[q] = A.x;
-      x[q] = __longlong_as_double((long long)A.y);
-      meta[q] = B[q].z;
-    }
-#pragma unroll
-    for (int q = 0; q < kILP; q++) {
-      // rank = r0 + (r + u) * drho, ref/darthash.py:282 (separately rounded)
-      int nu = meta[q] & 0xff, rho = (meta[q] >> 8) & 0xff;
-      double u = u53(finalize(pa[q] ^ T.js[j[q]][kStreamU - 1]));
-      double r0 = __dadd_rn(pow2(rho), -1.0);
-      rank[q] = __dadd_rn(r0, __dmul_rn(__dadd_rn((double)B[q].y, u), pow2(rho - nu)));
-      bool h = valid[q];
-      if (meta[q] & kArRb) h = h && rank[q] <= P.L_hi;  // interior rows pass by monotonicity
-      if (meta[q] & kArLb) h = h && rank[q] > P.L_lo;   // band: exclude darts seen before
-      needv[q] = h && (kFull || (meta[q] & kArWb));     // only the w_hi column can miss
-      hit[q] = h;
-    }
-    double weight[kILP];
-    bool anyv = false;
-#pragma unroll
-    for (int q = 0; q < kILP; q++) {
-      weight[q] = 0.0;
-      anyv = anyv || needv[q];
-    }
-    if (__any_sync(DSK_FULL, anyv)) {
-#pragma unroll
-      for (int q = 0; q < kILP; q++) {
-        int nu = meta[q] & 0xff, rho = (meta[q] >> 8) & 0xff;
-        double v = u53(finalize(pa[q] ^ T.js[j[q]][kStreamV - 1]));
-        double dnu = __dmul_rn(P.inv_t, pow2(nu - rho));
-        // weight = w0 + (w + v) * dnu, ref/darthash.py:281
-        weight[q] = __dadd_rn(T.w0[nu], __dmul_rn(__dadd_rn((double)B[q].x, v), dnu));
-        if (needv[q] && (meta[q] & kArWb)) hit[q] = weight[q] <= x[q];  // inclusive, :284
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < kILP; q++) {
-      if (kFull) {  // materialising sink: every hit with its full index tuple
-        if (hit[q]) {
-          DartRow d;
-          d.elem = B[q].w;
-          d.nu = meta[q] & 0xff;
-          d.rho = (meta[q] >> 8) & 0xff;
-          d.w = B[q].x;
-          d.r = B[q].y;
-          d.j = j[q];
-          d.weight = weight[q];
-          d.rank = rank[q];
-          d.fp = finalize(pa[q] ^ T.js[j[q]][kStreamFp - 1]);
-          sink.row(d);
-          n_hits++;
-        }
-      } else {
-        push_hit(hit[q], rank[q], pa[q] ^ T.js[j[q]][kStreamFp - 1]);
-      }
-    }
+    const uint32_t pos = lo + lane;
+    const bool valid = pos < hi;
+    const int src = warp_owner(hs.excl, pos);
+    const int ai = ringR(ar_head + src);
+    const ulonglong2 A = Q.arA[ai];
+    const uint4 B = Q.arB[ai];
+    const uint32_t meta = B.z;
+    const uint32_t j = ((pos - __shfl_sync(DSK_FULL, hs.excl, src)) +
+                        ((meta & kArJ1) ? 1u : 0u)) & (kJs - 1);
+    const double u = u53(finalize(A.x ^ T.js[j][kStreamU - 1]));
+    finish_dart(valid, A.x, meta, B.x, B.y, __longlong_as_double((long long)A.y), j, u, B.w);
     int npop;
     head_pop(hs, hi, lane, npop, ar_cur);
     ar_head = ringR(ar_head + npop);
@@ -415,7 +422,7 @@ struct Engine {
   // (ref/darthash.py:248-262), with the Poisson(1) count of each
   // (ref/randomness.py:145-147, :209-211: j = 0, stream 3)
   __device__ void regions_step() {
-    DSK_CHECK(ar_cnt < 32);
+    DSK_CHECK(ar_cnt < 32 && ht_cnt < kStep);
     const int mp = rg_cnt < 32 ? rg_cnt : 32;
     uint32_t c = 0;
     if (lane < mp) {
@@ -455,7 +462,6 @@ struct Engine {
       w[q] = ww;
       r[q] = rlo[q] + (off - ww * rc);
     }
-    uint32_t cnt[kILP];
 #pragma unroll
     for (int q = 0; q < kILP; q++) {
       uint64_t p = pa[q];
@@ -470,18 +476,12 @@ struct Engine {
                __ldg(&P.gtab[16 * 256 + ((r[q] >> 16) & 0xff)]) ^
                __ldg(&P.gtab[17 * 256 + (r[q] >> 24)]);
       }
-      pa[q] = p;
-      uint32_t k = poisson_count(finalize(p ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
-      cnt[q] = valid[q] ? k : 0;
-    }
-#pragma unroll
-    for (int q = 0; q < kILP; q++) {
-      bool lb = (rmeta[q] & kRgHasPrev) && r[q] == rlo[q];
-      if (!lb) n_darts += cnt[q];
-      uint32_t meta = (rmeta[q] & 0xffff) | (cnt[q] << 16) |
-                      (w[q] == whi[q] && (rmeta[q] & kRgWEdge) ? kArWb : 0) |
-                      (r[q] == rhi[q] ? kArRb : 0) | (lb ? kArLb : 0);
-      push_area(cnt[q] > 0, pa[q], x[q], w[q], r[q], meta, kFull ? rmeta[q] >> 20 : 0);
+      const bool lb = (rmeta[q] & kRgHasPrev) && r[q] == rlo[q];
+      const uint32_t meta = (rmeta[q] & 0xffff) |
+                            (w[q] == whi[q] && (rmeta[q] & kRgWEdge) ? kArWb : 0) |
+                            (r[q] == rhi[q] ? kArRb : 0) | (lb ? kArLb : 0);
+      emit_area<Sink::kFuse && DSK_FUSE >= 2>(valid[q], p, x[q], w[q], r[q], meta, lb,
+                               kFull ? rmeta[q] >> 20 : 0);
     }
     int npop;
     head_pop(hs, hi, lane, npop, rg_cur);
@@ -555,7 +555,7 @@ struct Engine {
   }
 
   __device__ void direct_step() {
-    DSK_CHECK(ar_cnt < 32);
+    DSK_CHECK(ar_cnt < 32 && ht_cnt < kStep);
     // refill idle walkers with the chunk's next runs
     bool idle = wk_a >= wk_end;
     unsigned idle_mask = __ballot_sync(DSK_FULL, idle);
@@ -581,15 +581,12 @@ struct Engine {
     const uint32_t r = wk_r;
     uint64_t p = el.x ^ T.tNu[nu] ^ T.tRho[0] ^ T.tW[0][0] ^ T.tW[1][0] ^ T.cfold ^
                  T.tR[0][r & 0xff] ^ T.tR[1][(r >> 8) & 0xff];
-    uint32_t k = poisson_count(finalize(p ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
-    uint32_t cnt = act ? k : 0;
     const bool hp = (wk_rlo & 0x80000000u) != 0;
     const bool lb = hp && r == (wk_rlo & 0x7fffffffu);
-    if (!lb) n_darts += cnt;
-    uint32_t meta = (uint32_t)nu | (cnt << 16) | (nu >= (int)(d.y >> 8) ? kArWb : 0) |
-                    (r == wk_rhi ? kArRb : 0) | (lb ? kArLb : 0);
-    push_area(cnt > 0, p, __longlong_as_double((long long)el.y), 0, r, meta,
-              kFull ? Q.elIdx[wk_slot] : 0);
+    const uint32_t meta = (uint32_t)nu | (nu >= (int)(d.y >> 8) ? kArWb : 0) |
+                          (r == wk_rhi ? kArRb : 0) | (lb ? kArLb : 0);
+    emit_area<Sink::kFuse && DSK_FUSE >= 1>(act, p, __longlong_as_double((long long)el.y), 0, r, meta, lb,
+                             kFull ? Q.elIdx[wk_slot] : 0);
     // advance: next row, else the next non-empty nu
     if (act) {
       wk_a++;

@@ -158,6 +158,7 @@ __device__ __forceinline__ void team_sync(int G, int team) {
 // ------------------------------------------------------------- minhash
 
 struct MinhashSink {
+  static constexpr bool kFuse = true;
   uint64_t *slots;  // 2*k words: {rank bits, fingerprint} per slot, 16-B aligned
   ModU32 md;
   unsigned int *filled;
@@ -461,6 +462,7 @@ struct DartsArgs {
 };
 
 struct RowSink {
+  static constexpr bool kFuse = true;
   const DartsArgs *a;
   int64_t set, lo;
   unsigned long long *cursor;  // shared per warp

@@ -19,6 +19,7 @@
 //   epilogue     one lane per table folds the K fingerprints with mix64.
 
 struct LshSink {
+  static constexpr bool kFuse = false;
   ulonglong2 *buf;      // global: {fp, rank bits} per buffered hit
   uint32_t *bkt;        // global: bucket per buffered hit
   uint32_t cap;
