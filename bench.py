@@ -343,6 +343,15 @@ def main():
         cpu = cpu_baseline(cfg, k, indptr, ids, w, args.cpu_seconds, cfg.L, cfg.K)
 
     if rank == 0:
+        traffic = None
+        tkey = cfg.name if args.k is None else f"{cfg.name}_k{k}"
+        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath) and args.sets is None:
+            entry = json.load(open(tpath)).get(tkey)
+            if entry:
+                traffic = {"bytes_per_launch": entry["bytes_per_launch"],
+                           "algorithmic_bytes_per_launch": hbm_bytes,
+                           "source": entry["source"]}
         achieved = hashes_all / sec / 1e9
         peak = peak_hps / 1e9
         line = {
@@ -358,7 +367,7 @@ def main():
             "darts_per_sec": hits_all / sec,
             "hash_evals_per_sec": hashes_all / sec,
             "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
-                         "unit": "Ghash/s", "frac": achieved / peak, "traffic": None,
+                         "unit": "Ghash/s", "frac": achieved / peak, "traffic": traffic,
                          "peak_hoisted": peak_hoisted_hps / 1e9,
                          "frac_hoisted": achieved / (peak_hoisted_hps / 1e9),
                          "note": "achieved = algorithmic hash evaluations A+2D+2H per set "

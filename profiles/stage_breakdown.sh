@@ -1,7 +1,7 @@
 #!/bin/bash
 # usage: profiles/stage_breakdown.sh <ncu-rep>   (per-engine-stage share of instructions/stalls)
 REP=$1
-python "$(dirname "$0")/sass_lines.py" "$REP" _Z14minhash_kernel11MinhashArgs paper_2005_11547_b200/libdsk_b200.so 600 dsk_engine.cuh > /tmp/eng_lines.txt
+python "$(dirname "$0")/sass_lines.py" "$REP" ${KNAME:-_Z14minhash_kernelILi22EEv11MinhashArgs} paper_2005_11547_b200/libdsk_b200.so 600 dsk_engine.cuh > /tmp/eng_lines.txt
 python - "$(dirname "$0")/../paper_2005_11547_b200/csrc/dsk_engine.cuh" <<'PY'
 import re, sys
 src = open(sys.argv[1]).read().splitlines()
