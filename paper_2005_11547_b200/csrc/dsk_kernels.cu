@@ -30,6 +30,8 @@ using namespace dsk;
 
 // ------------------------------------------------------------- context
 
+constexpr int kMaxChunks = 64;  // host-buffer pipeline chunks per call
+
 struct dsk_ctx {
   int device;
   int num_sms;
@@ -43,8 +45,8 @@ struct dsk_ctx {
   std::mutex host_mu;
   void *stage = nullptr;
   size_t stage_bytes = 0;
-  cudaStream_t hs[2] = {nullptr, nullptr};
-  cudaEvent_t ev_in[2] = {nullptr, nullptr};
+  cudaStream_t hs[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_in[kMaxChunks] = {}, ev_k[kMaxChunks] = {};
   // LSH hit buffers (one slice per resident team)
   std::mutex scratch_mu;
   void *lsh_scratch = nullptr;
@@ -717,9 +719,11 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
   cudaFree(c->d_counter);
   if (c->stage) cudaFree(c->stage);
   if (c->lsh_scratch) cudaFree(c->lsh_scratch);
-  for (int i = 0; i < 2; i++) {
+  for (int i = 0; i < 4; i++)
     if (c->hs[i]) cudaStreamDestroy(c->hs[i]);
+  for (int i = 0; i < kMaxChunks; i++) {
     if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
+    if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
   }
   delete c;
   return DSK_OK;
@@ -876,46 +880,102 @@ extern "C" int dsk_hash_peak(dsk_ctx *c, int32_t mode, int64_t n_per_thread, uin
 // ------------------------------------------------------ host-buffer calls
 //
 // dsk_*_csr_host: the drop-in for a caller holding numpy arrays.  Rows are
-// cut into chunks of ~128 MB of input; chunk c is copied in, sketched and
-// copied out on stream c % 2, so the PCIe transfers of one chunk overlap the
-// kernel of the other.  Device staging is owned by the context and reused.
+// cut into chunks; one copy stream issues every chunk's H2D back to back
+// (the whole input is staged, so the copy engine never waits), the compute
+// streams run chunk c's kernel once its input event fires, and an output
+// stream copies chunk c's results back once its kernel event fires.  The
+// PCIe H2D then runs without gaps and only the last chunk's kernel and D2H
+// stick out, so chunks ramp up at the start (16, 32 MB) and halve towards
+// the end (down to 8 MB).  Device staging is owned by the context.
 
 static int ensure_stage(dsk_ctx *c, size_t bytes) {
+  if (!c->hs[0]) {
+    for (int i = 0; i < 4; i++)
+      CUDA_TRY(cudaStreamCreateWithFlags(&c->hs[i], cudaStreamNonBlocking));
+    for (int i = 0; i < kMaxChunks; i++) {
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_k[i], cudaEventDisableTiming));
+    }
+  }
   if (c->stage_bytes >= bytes) return DSK_OK;
   if (c->stage) CUDA_TRY(cudaFree(c->stage));
   c->stage = nullptr;
   c->stage_bytes = 0;
   CUDA_TRY(cudaMalloc(&c->stage, bytes));
   c->stage_bytes = bytes;
-  if (!c->hs[0]) {
-    for (int i = 0; i < 2; i++) {
-      CUDA_TRY(cudaStreamCreateWithFlags(&c->hs[i], cudaStreamNonBlocking));
-      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming));
-    }
-  }
   return DSK_OK;
 }
 
-// Row chunk boundaries with ~target input bytes per chunk.
-static void plan_chunks(const int64_t *indptr, int64_t n, size_t target, int64_t *bounds,
+// Row chunk boundaries: chunk i carries ~min(cap, 16 MB << i, max(8 MB,
+// remaining / 2)) input bytes (16 B per nonzero + 8 B per row).
+static void plan_chunks(const int64_t *indptr, int64_t n, size_t cap, int64_t *bounds,
                         int max_chunks, int *nchunks) {
+  const size_t total = (size_t)indptr[n] * 16 + (size_t)n * 8;
+  if (cap < total / (max_chunks - 12)) cap = total / (max_chunks - 12) + 1;
   int m = 0;
   bounds[m++] = 0;
   int64_t r = 0;
+  size_t done = 0;
   while (r < n && m < max_chunks) {
-    int64_t lo = r;
-    // advance until ~target bytes (16 B per nonzero + 8 B per row)
+    const int64_t lo = r;
+    size_t target = cap;
+    const size_t ramp = (size_t)16 << (20 + (m - 1 < 6 ? m - 1 : 6));
+    if (ramp < target) target = ramp;
+    size_t half = (total - done) / 2;
+    if (half < ((size_t)8 << 20)) half = (size_t)8 << 20;
+    if (half < target) target = half;
     int64_t step = 1;
     while (r < n && (size_t)((indptr[r] - indptr[lo]) * 16 + (r - lo) * 8) < target) {
-      int64_t nr = r + step < n ? r + step : n;
-      r = nr;
+      r = r + step < n ? r + step : n;
       step = step < (1 << 16) ? step * 2 : step;
     }
     if (r == lo) r = lo + 1;
+    done += (size_t)((indptr[r] - indptr[lo]) * 16 + (r - lo) * 8);
     bounds[m++] = r;
   }
   if (bounds[m - 1] != n) bounds[m - 1] = n;
   *nchunks = m - 1;
+}
+
+static size_t host_chunk_cap() {
+  size_t mb = 64;  // measured on cfg2: 64 MB 32.1 ms/step e2e, 128 MB 32.8, 256 MB 34.8
+  if (const char *e = getenv("DSK_CHUNK_MB")) mb = atoi(e) > 0 ? (size_t)atoi(e) : 64;
+  return mb << 20;
+}
+
+// Drive the pipeline.  launch(r0, m, stream) sketches rows [r0, r0 + m)
+// reading the staged input; out(r0, m, stream) copies their results back.
+// dp/di/dw are the staged indptr/ids/weights.  With two compute streams the
+// CTAs of chunk c + 1 take over SMs as chunk c's persistent CTAs retire, so
+// launch tails overlap (needs launches that share no scratch: minhash).
+template <class Launch, class Out>
+static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
+                         const double *weights, int64_t n, int64_t *dp, uint64_t *di, double *dw,
+                         int compute_streams, Launch launch, Out out) {
+  int64_t bounds[kMaxChunks + 1];
+  int nch = 0;
+  plan_chunks(indptr, n, host_chunk_cap(), bounds, kMaxChunks + 1, &nch);
+  cudaStream_t cp = c->hs[0], os = c->hs[2];
+  CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, cp));
+  for (int ch = 0; ch < nch; ch++) {
+    const int64_t e0 = indptr[bounds[ch]], e1 = indptr[bounds[ch + 1]];
+    CUDA_TRY(cudaMemcpyAsync(di + e0, ids + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, cp));
+    CUDA_TRY(cudaMemcpyAsync(dw + e0, weights + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, cp));
+    CUDA_TRY(cudaEventRecord(c->ev_in[ch], cp));
+  }
+  int rc = DSK_OK;
+  for (int ch = 0; ch < nch && rc == DSK_OK; ch++) {
+    const int64_t r0 = bounds[ch], m = bounds[ch + 1] - r0;
+    cudaStream_t ks = c->hs[(compute_streams > 1 && (ch & 1)) ? 3 : 1];
+    CUDA_TRY(cudaStreamWaitEvent(ks, c->ev_in[ch], 0));
+    rc = launch(r0, m, ks);
+    if (rc) break;
+    CUDA_TRY(cudaEventRecord(c->ev_k[ch], ks));
+    CUDA_TRY(cudaStreamWaitEvent(os, c->ev_k[ch], 0));
+    rc = out(r0, m, os);
+  }
+  for (int i = 0; i < 4; i++) CUDA_TRY(cudaStreamSynchronize(c->hs[i]));
+  return rc;
 }
 
 extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
@@ -948,25 +1008,12 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
   int32_t *ds = (int32_t *)(base + off_s);
   int32_t *dph = phi ? (int32_t *)(base + off_ph) : nullptr;
   uint32_t *dst = stats ? (uint32_t *)(base + off_st) : nullptr;
-  constexpr int kMaxChunks = 64;
-  int64_t bounds[kMaxChunks + 1];
-  int nch = 0;
-  size_t chunk_mb = 128;  // ~2 ms of PCIe per chunk: balances copy and kernel time
-  if (const char *e = getenv("DSK_CHUNK_MB")) chunk_mb = (size_t)atoi(e) > 0 ? (size_t)atoi(e) : 128;
-  plan_chunks(indptr, n, chunk_mb << 20, bounds, kMaxChunks + 1, &nch);
-  CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, c->hs[0]));
-  CUDA_TRY(cudaEventRecord(c->ev_in[0], c->hs[0]));
-  CUDA_TRY(cudaStreamWaitEvent(c->hs[1], c->ev_in[0], 0));
-  for (int ch = 0; ch < nch; ch++) {
-    cudaStream_t st = c->hs[ch & 1];
-    int64_t r0 = bounds[ch], r1 = bounds[ch + 1], m = r1 - r0;
-    int64_t e0 = indptr[r0], e1 = indptr[r1];
-    CUDA_TRY(cudaMemcpyAsync(di + e0, ids + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(dw + e0, weights + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, st));
-    rc = dsk_minhash_csr(c, dp + r0, di, dw, m, k, dv ? dv + r0 * k : nullptr,
-                         db ? db + r0 * words : nullptr, ds + r0, dph ? dph + r0 : nullptr,
-                         dst ? dst + r0 * 4 : nullptr, st);
-    if (rc) return rc;
+  auto launch = [&](int64_t r0, int64_t m, cudaStream_t st) {
+    return dsk_minhash_csr(c, dp + r0, di, dw, m, k, dv ? dv + r0 * k : nullptr,
+                           db ? db + r0 * words : nullptr, ds + r0, dph ? dph + r0 : nullptr,
+                           dst ? dst + r0 * 4 : nullptr, st);
+  };
+  auto out = [&](int64_t r0, int64_t m, cudaStream_t st) -> int {
     if (out_values)
       CUDA_TRY(cudaMemcpyAsync(out_values + r0 * k, dv + r0 * k, (size_t)m * k * 8,
                                cudaMemcpyDeviceToHost, st));
@@ -977,10 +1024,11 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
     if (phi) CUDA_TRY(cudaMemcpyAsync(phi + r0, dph + r0, m * 4, cudaMemcpyDeviceToHost, st));
     if (stats)
       CUDA_TRY(cudaMemcpyAsync(stats + r0 * 4, dst + r0 * 4, m * 16, cudaMemcpyDeviceToHost, st));
-  }
-  CUDA_TRY(cudaStreamSynchronize(c->hs[0]));
-  CUDA_TRY(cudaStreamSynchronize(c->hs[1]));
-  return DSK_OK;
+    return DSK_OK;
+  };
+  int streams = 2;
+  if (const char *e = getenv("DSK_HOST_STREAMS")) streams = atoi(e) == 1 ? 1 : 2;
+  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, streams, launch, out);
 }
 
 #include "dsk_lsh_host.cuh"

@@ -77,18 +77,23 @@ extern "C" int dsk_lsh_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_
   int32_t *ds = (int32_t *)(base + off_s);
   int32_t *dph = phi ? (int32_t *)(base + off_ph) : nullptr;
   uint32_t *dst = stats ? (uint32_t *)(base + off_st) : nullptr;
-  cudaStream_t st = c->hs[0];
-  CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(di, ids, nnz * 8, cudaMemcpyHostToDevice, st));
-  CUDA_TRY(cudaMemcpyAsync(dw, weights, nnz * 8, cudaMemcpyHostToDevice, st));
-  rc = dsk_lsh_csr(c, dp, di, dw, n, L, K, normalize, dk, df, ds, dph, dst, st);
-  if (rc) return rc;
-  if (out_keys) CUDA_TRY(cudaMemcpyAsync(out_keys, dk, (size_t)n * L * 8, cudaMemcpyDeviceToHost, st));
-  if (out_fps)
-    CUDA_TRY(cudaMemcpyAsync(out_fps, df, (size_t)n * L * K * 8, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaMemcpyAsync(status, ds, n * 4, cudaMemcpyDeviceToHost, st));
-  if (phi) CUDA_TRY(cudaMemcpyAsync(phi, dph, n * 4, cudaMemcpyDeviceToHost, st));
-  if (stats) CUDA_TRY(cudaMemcpyAsync(stats, dst, n * 16, cudaMemcpyDeviceToHost, st));
-  CUDA_TRY(cudaStreamSynchronize(st));
-  return DSK_OK;
+  auto launch = [&](int64_t r0, int64_t m, cudaStream_t st) {
+    return dsk_lsh_csr(c, dp + r0, di, dw, m, L, K, normalize, dk ? dk + r0 * L : nullptr,
+                       df ? df + r0 * L * K : nullptr, ds + r0, dph ? dph + r0 : nullptr,
+                       dst ? dst + r0 * 4 : nullptr, st);
+  };
+  auto out = [&](int64_t r0, int64_t m, cudaStream_t st) -> int {
+    if (out_keys)
+      CUDA_TRY(cudaMemcpyAsync(out_keys + r0 * L, dk + r0 * L, (size_t)m * L * 8,
+                               cudaMemcpyDeviceToHost, st));
+    if (out_fps)
+      CUDA_TRY(cudaMemcpyAsync(out_fps + r0 * L * K, df + r0 * L * K, (size_t)m * L * K * 8,
+                               cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(status + r0, ds + r0, m * 4, cudaMemcpyDeviceToHost, st));
+    if (phi) CUDA_TRY(cudaMemcpyAsync(phi + r0, dph + r0, m * 4, cudaMemcpyDeviceToHost, st));
+    if (stats)
+      CUDA_TRY(cudaMemcpyAsync(stats + r0 * 4, dst + r0 * 4, m * 16, cudaMemcpyDeviceToHost, st));
+    return DSK_OK;
+  };
+  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, 1, launch, out);  // shared scratch
 }

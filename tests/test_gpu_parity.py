@@ -389,6 +389,38 @@ def test_lsh_host_buffer_abi():
     assert np.array_equal(keys, as_u64(dev.keys))
 
 
+@pytest.mark.parametrize("chunk_mb", ["1", "3"])
+def test_host_pipeline_many_chunks(monkeypatch, chunk_mb):
+    """Small chunk caps: many chunks through the three-stream pipeline (input
+    events, kernel events, D2H stream) for both host entry points."""
+    import ctypes
+
+    from paper_2005_11547_b200 import _lib
+    monkeypatch.setenv("DSK_CHUNK_MB", chunk_mb)
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+    indptr, ids, w = workloads.generate("cfg3", n=6000)
+    f = fam(2)
+    dev = minhash_batch(indptr, ids, w, 64, f)
+    vals = np.zeros((6000, 64), dtype=np.uint64)
+    status = np.full(6000, -1, dtype=np.int32)
+    rc = _lib.load().dsk_minhash_csr_host(f.context(), P(indptr), P(ids), P(w), 6000, 64, P(vals),
+                                         None, P(status), None, None)
+    assert rc == 0 and (status == 0).all()
+    assert np.array_equal(vals, as_u64(dev.values))
+    indptr, ids, w = workloads.generate("cfg4", n=1500)
+    dev = lsh_batch(indptr, ids, w, LshParams(30, 4), f, fps=True)
+    keys = np.zeros((1500, 30), dtype=np.uint64)
+    fps = np.zeros((1500, 30, 4), dtype=np.uint64)
+    status = np.full(1500, -1, dtype=np.int32)
+    phi = np.zeros(1500, dtype=np.int32)
+    rc = _lib.load().dsk_lsh_csr_host(f.context(), P(indptr), P(ids), P(w), 1500, 30, 4, 0,
+                                     P(keys), P(fps), P(status), P(phi), None)
+    assert rc == 0 and (status == 0).all()
+    assert np.array_equal(keys, as_u64(dev.keys))
+    assert np.array_equal(fps, as_u64(dev.fps))
+    assert np.array_equal(phi, dev.phi.cpu().numpy())
+
+
 def test_tie_resolution_path():
     """Rows flagged DSK_STATUS_TIE are re-resolved by full index tuple on the
     GPU (ref/sketching.py:93-99); force the path on corrupted rows."""
