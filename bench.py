@@ -303,22 +303,26 @@ def main():
 
     # e2e through the C ABI with host (pinned) buffers
     e2e = None
-    if not args.no_e2e and cfg.kind != "lsh":
+    if not args.no_e2e:
         pin_p = torch.from_numpy(indptr).pin_memory()
         pin_i = torch.from_numpy(ids.view(np.int64)).pin_memory()
         pin_w = torch.from_numpy(w).pin_memory()
-        o_v = torch.empty((n, k), dtype=torch.int64).pin_memory()
+        lsh = cfg.kind == "lsh"
+        o_v = torch.empty((n, cfg.L if lsh else k), dtype=torch.int64).pin_memory()
         o_s = torch.empty(n, dtype=torch.int32).pin_memory()
         words = (k + 63) // 64
         o_b = torch.empty((n, words), dtype=torch.int64).pin_memory() if onebit else None
+        api = "dsk_lsh_csr_host" if lsh else "dsk_minhash_csr_host"
+        P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
 
         def host_call():
-            rc = lib.dsk_minhash_csr_host(
-                ctx, ctypes.c_void_p(pin_p.data_ptr()), ctypes.c_void_p(pin_i.data_ptr()),
-                ctypes.c_void_p(pin_w.data_ptr()), n, k, ctypes.c_void_p(o_v.data_ptr()),
-                ctypes.c_void_p(o_b.data_ptr()) if o_b is not None else None,
-                ctypes.c_void_p(o_s.data_ptr()), None, None)
-            _lib.check(rc, "dsk_minhash_csr_host")
+            if lsh:
+                rc = lib.dsk_lsh_csr_host(ctx, P(pin_p), P(pin_i), P(pin_w), n, cfg.L, cfg.K, 0,
+                                          P(o_v), None, P(o_s), None, None)
+            else:
+                rc = lib.dsk_minhash_csr_host(ctx, P(pin_p), P(pin_i), P(pin_w), n, k, P(o_v),
+                                              P(o_b), P(o_s), None, None)
+            _lib.check(rc, api)
 
         host_call()
         if world > 1:
@@ -335,7 +339,7 @@ def main():
         d2h = o_v.numel() * 8 + o_s.numel() * 4 + (o_b.numel() * 8 if o_b is not None else 0)
         e2e = {"value": sets_all / dt, "unit": "sketches/sec", "ms_per_step": dt * 1000.0,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "api": "dsk_minhash_csr_host (C ABI, pinned host buffers)"}
+               "api": f"{api} (C ABI, pinned host buffers)"}
         assert (o_s.numpy() == 0).all()
 
     cpu = None

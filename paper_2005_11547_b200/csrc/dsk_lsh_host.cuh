@@ -35,7 +35,9 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
   LshArgs a;
   a.indptr = indptr; a.ids = ids; a.w = weights; a.n = n; a.L = L; a.K = K;
-  a.normalize = normalize; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
+  a.normalize = normalize;
+  const char *ex = getenv("DSK_LSH_EXACT");
+  a.exact_sort = ex && atoi(ex) != 0; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
   a.md = make_mod((uint32_t)L); a.G = G; a.out_keys = out_keys; a.out_fps = out_fps;
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
   a.scratch = (unsigned char *)c->lsh_scratch; a.team_scratch = team_bytes; a.cap = cap;

@@ -1,4 +1,7 @@
 // dsk_lsh_kernel.cuh -- K5: (L, K) LSH table keys (included by dsk_kernels.cu).
+#ifndef DSK_LSH_FAST
+#define DSK_LSH_FAST 1  // 0: exact sort only; 1: float-key sort + exact fallback; 2: timing only
+#endif
 //
 // lsh_key (ref/annindex.py:64-82): density t = L*K; darts are bucketed by
 // hash64(fp, stream 5) mod L; at the first phi step where every bucket holds
@@ -58,6 +61,7 @@ struct LshArgs {
   int64_t n;
   int32_t L, K;
   int32_t normalize;
+  int32_t exact_sort;  // 1: skip the float-key fast path (env DSK_LSH_EXACT=1; tests)
   double tf, inv_t;
   ModU32 md;
   int G;
@@ -209,14 +213,70 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       __threadfence_block();
       team_sync(G, team);
       // K smallest of each bucket by (rank bits, fp).  Buckets of <= 64
-      // entries (nearly all: ~2K per bucket at the stopping step) are sorted
-      // in registers with a 64-wide bitonic network; larger ones rank each
-      // entry by counting.  Bit-identical ranks with different fingerprints
-      // flag a tie (the reference orders them by index tuple).
+      // entries (nearly all: ~40 per bucket at cfg4's stopping step) are
+      // sorted in registers with a 64-wide bitonic network, first on a packed
+      // {float rank, buffer index} key and, if two of the first K + 1 float
+      // ranks coincide, again on the exact (rank bits, fp) pair; larger
+      // buckets rank each entry by counting.  Bit-identical ranks with
+      // different fingerprints flag a tie (the reference orders them by
+      // index tuple).
       bool tie = false;
       for (int b = wit; b < L; b += G) {
         const unsigned o = off[b], nb = cnt[b];
-        if (nb <= 64) {
+        bool exact = nb > 64 || DSK_LSH_FAST == 0 || a.exact_sort;
+        if (!exact) {
+          // fast path: bitonic sort of one 64-bit key per entry, the rank
+          // rounded to float (monotone) above the entry's buffer index; when
+          // the first K + 1 sorted keys have distinct float ranks their order
+          // and the K-set equal the exact (rank, fp) order, else the bucket
+          // takes the exact path below
+          unsigned long long key[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            unsigned i = lane + 32 * h;
+            if (i < nb) {
+              uint32_t ei = order[o + i];
+              double rk = __longlong_as_double((long long)buf[ei].y);
+              key[h] = ((unsigned long long)__float_as_uint(__double2float_rn(rk)) << 32) | ei;
+            } else {
+              key[h] = ~0ULL;
+            }
+          }
+          for (int kk = 2; kk <= 64; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+              if (j == 32) {
+                if (key[1] < key[0]) { unsigned long long t0 = key[0]; key[0] = key[1]; key[1] = t0; }
+              } else {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                  int p = lane + 32 * h;
+                  unsigned long long y = __shfl_xor_sync(DSK_FULL, key[h], j);
+                  bool take_min = ((p & j) == 0) == ((p & kk) == 0);
+                  if (take_min == (y < key[h])) key[h] = y;
+                }
+              }
+            }
+          }
+          unsigned long long d0 = __shfl_down_sync(DSK_FULL, key[0], 1);
+          unsigned long long f1 = __shfl_sync(DSK_FULL, key[1], 0);
+          unsigned long long d1 = __shfl_down_sync(DSK_FULL, key[1], 1);
+          unsigned long long nx[2] = {lane < 31 ? d0 : f1, d1};
+          bool coll = false;
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            unsigned p = lane + 32 * h;
+            if (p < (unsigned)K && p + 1 < nb && (nx[h] >> 32) == (key[h] >> 32)) coll = true;
+          }
+          exact = __any_sync(DSK_FULL, coll) && DSK_LSH_FAST == 1;
+          if (!exact) {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              unsigned p = lane + 32 * h;
+              if (p < (unsigned)K && p < nb) sel[(size_t)b * K + p] = buf[(uint32_t)key[h]].x;
+            }
+          }
+        }
+        if (exact && nb <= 64) {
           unsigned long long kr[2], kf[2];
 #pragma unroll
           for (int h = 0; h < 2; h++) {
@@ -266,7 +326,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
             if (p + 1 < nb && nxr[h] == kr[h] && nxf[h] != kf[h]) tie = true;
             if (p < (unsigned)K) sel[(size_t)b * K + p] = kf[h];
           }
-        } else {
+        } else if (exact) {
           for (unsigned i = lane; i < nb; i += 32) {
             uint32_t ei = order[o + i];
             ulonglong2 e = buf[ei];

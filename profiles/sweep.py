@@ -15,10 +15,9 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "fuse2": {},
-    "fuse1": {"DSK_FUSE": 1},
-    "fuse0": {"DSK_FUSE": 0},
-    "fuse2d1": {"DSK_DIRECT": 1},
+    "lf1": {},
+    "lf0": {"DSK_LSH_FAST": 0},
+    "lf2": {"DSK_LSH_FAST": 2},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]

@@ -307,6 +307,28 @@ def test_lsh_small_shapes():
         assert np.array_equal(as_u64(res.fps), g[f"fps_{L}_{K}"]), (L, K)
 
 
+@pytest.mark.parametrize("scale_exp", [None, -200])
+def test_lsh_sort_paths_agree(monkeypatch, scale_exp):
+    """The float-key bucket sort and the exact (rank, fp) sort give the same
+    keys.  With ||x||_1 = 2^-200 nearly every rank exceeds the float range,
+    so every bucket collides on its float keys and takes the exact path."""
+    indptr, ids, w = workloads.generate("cfg4", n=300, start=777)
+    if scale_exp is not None:
+        for s in range(indptr.size - 1):
+            a, b = indptr[s], indptr[s + 1]
+            w[a:b] = np.ldexp(w[a:b] / w[a:b].sum(), scale_exp)
+    f = fam(3)
+    fast = lsh_batch(indptr, ids, w, LshParams(50, 8), f, fps=True)
+    monkeypatch.setenv("DSK_LSH_EXACT", "1")
+    exact = lsh_batch(indptr, ids, w, LshParams(50, 8), f, fps=True)
+    assert np.array_equal(as_u64(fast.keys), as_u64(exact.keys))
+    assert np.array_equal(as_u64(fast.fps), as_u64(exact.fps))
+    keys, fps, status, _, _ = Oracle(3).lsh_csr(indptr, ids, w, 50, 8, want_fps=True)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(fast.keys), keys)
+    assert np.array_equal(as_u64(fast.fps), fps)
+
+
 def test_lsh_cfg4_vs_oracle():
     indptr, ids, w = workloads.generate("cfg4", n=400, start=5000)
     f = fam(3)
