@@ -749,7 +749,9 @@ static bool team_size_ok(int G, int nw) { return nw % G == 0 && (G == 1 || nw / 
 template <class SmemFn>
 static bool choose_shape(const dsk_ctx *c, SmemFn smem_of, int &nw_out, int &g_out) {
   int best_g = 1 << 30, best_nw = 0;
+  const char *force = getenv("DSK_NW");  // tuning: restrict to one CTA width
   for (int nw : kWidths) {
+    if (force && atoi(force) != nw) continue;
     for (int G = 1; G <= nw; G++) {
       if (!team_size_ok(G, nw) || smem_of(G, nw) > c->max_smem) continue;
       if (G < best_g) { best_g = G; best_nw = nw; }

@@ -187,6 +187,46 @@ def test_minhash_cfg3_vs_oracle(k):
     _oracle_compare("cfg3", k, {64: 4000, 256: 2000, 1024: 600}[k], start=70000, bits=True)
 
 
+def _ragged_batch(seed, lens, sigma=2.0, d=1 << 26):
+    rng = np.random.default_rng(seed)
+    lens = np.asarray(lens, dtype=np.int64)
+    indptr = np.zeros(lens.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    ids = np.concatenate([rng.choice(d, int(m), replace=False).astype(np.uint64) if m else
+                          np.zeros(0, np.uint64) for m in lens])
+    w = rng.lognormal(0.0, sigma, int(indptr[-1]))
+    return indptr, ids, w
+
+
+def test_minhash_max_sizes_and_ragged_vs_oracle():
+    """cfg5's extremes: sets at its nnz clip (16384) and beyond, single-element
+    and empty sets in one ragged batch (per-set status for the empty ones)."""
+    lens = [16384, 0, 1, 16384, 2, 3000, 0, 65536, 1, 16383, 7, 16385]
+    indptr, ids, w = _ragged_batch(21, lens)
+    for k in (1, 128, 300):
+        res = minhash_batch(indptr, ids, w, k, fam(4), check=False)
+        vals, status, phi, hits = Oracle(4).minhash_csr(indptr, ids, w, k)
+        st = res.status.cpu().numpy()
+        assert np.array_equal(st, status), k
+        ok = status == 0
+        assert ok.sum() == len(lens) - 2
+        assert np.array_equal(as_u64(res.values)[ok], vals[ok]), k
+        assert np.array_equal(res.phi.cpu().numpy()[ok], phi[ok]), k
+        got_h = res.stats.cpu().numpy().view(np.uint32)[:, 2].astype(np.int64)
+        assert np.array_equal(got_h[ok], hits[ok]), k
+
+
+def test_lsh_max_sizes_vs_oracle():
+    lens = [16384, 1, 4000, 16384, 2, 20000]
+    indptr, ids, w = _ragged_batch(22, lens, sigma=1.0)
+    res = lsh_batch(indptr, ids, w, LshParams(100, 20), fam(3), fps=True)
+    keys, fps, status, phi, _ = Oracle(3).lsh_csr(indptr, ids, w, 100, 20, want_fps=True)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(as_u64(res.fps), fps)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+
+
 def test_minhash_cfg5_vs_oracle():
     _oracle_compare("cfg5", 128, 4000, start=200000)
 
