@@ -99,6 +99,10 @@ int dsk_lsh_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
                 uint64_t *out_keys, uint64_t *out_fps, int32_t *status, int32_t *phi,
                 uint32_t *stats, void *stream);
 
+/* Host-buffer form of dsk_lsh_csr (same pipeline as dsk_minhash_csr_host).
+ * LSH launches draw their per-team hit buffers from a pool of context-owned
+ * slots reused in stream order, so concurrent calls on different streams
+ * are safe. */
 int dsk_lsh_csr_host(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
                      const double *weights, int64_t n, int32_t L, int32_t K, int32_t normalize,
                      uint64_t *out_keys, uint64_t *out_fps, int32_t *status, int32_t *phi,

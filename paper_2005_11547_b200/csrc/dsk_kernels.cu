@@ -47,10 +47,14 @@ struct dsk_ctx {
   size_t stage_bytes = 0;
   cudaStream_t hs[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in[kMaxChunks] = {}, ev_k[kMaxChunks] = {};
-  // LSH hit buffers (one slice per resident team)
+  // LSH hit buffers (one slice per resident team), a small pool of slots
+  // reused in stream order: a launch waits for the previous user of its slot
   std::mutex scratch_mu;
-  void *lsh_scratch = nullptr;
-  size_t lsh_scratch_bytes = 0;
+  static constexpr int kLshSlots = 4;
+  void *lsh_scratch[kLshSlots] = {};
+  size_t lsh_scratch_bytes[kLshSlots] = {};
+  cudaEvent_t lsh_last[kLshSlots] = {};
+  unsigned lsh_next = 0;
 };
 
 constexpr int kCounterSlots = 256;
@@ -718,7 +722,10 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
   cudaFree(c->d_l2thr);
   cudaFree(c->d_counter);
   if (c->stage) cudaFree(c->stage);
-  if (c->lsh_scratch) cudaFree(c->lsh_scratch);
+  for (int i = 0; i < dsk_ctx::kLshSlots; i++) {
+    if (c->lsh_scratch[i]) cudaFree(c->lsh_scratch[i]);
+    if (c->lsh_last[i]) cudaEventDestroy(c->lsh_last[i]);
+  }
   for (int i = 0; i < 4; i++)
     if (c->hs[i]) cudaStreamDestroy(c->hs[i]);
   for (int i = 0; i < kMaxChunks; i++) {
@@ -949,7 +956,7 @@ static size_t host_chunk_cap() {
 // reading the staged input; out(r0, m, stream) copies their results back.
 // dp/di/dw are the staged indptr/ids/weights.  With two compute streams the
 // CTAs of chunk c + 1 take over SMs as chunk c's persistent CTAs retire, so
-// launch tails overlap (needs launches that share no scratch: minhash).
+// launch tails overlap (LSH launches take separate scratch slots).
 template <class Launch, class Out>
 static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                          const double *weights, int64_t n, int64_t *dp, uint64_t *di, double *dw,

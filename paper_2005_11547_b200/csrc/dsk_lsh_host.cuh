@@ -21,15 +21,27 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   uint32_t cap = (uint32_t)(8 * t > 16384 ? 8 * t : 16384);
   size_t team_bytes = align16((size_t)cap * 24) + align16((size_t)L * K * 8);
   size_t need = (size_t)grid * teams * team_bytes;
+  // scratch slot: stream-ordered reuse (waits for the slot's previous launch),
+  // so concurrent calls on different streams never share a hit buffer
+  // (the lock is held until the slot's event is recorded after the launch)
+  std::lock_guard<std::mutex> lock(c->scratch_mu);
+  int slot;
+  void *scratch;
   {
-    std::lock_guard<std::mutex> lock(c->scratch_mu);
-    if (c->lsh_scratch_bytes < need) {
-      if (c->lsh_scratch) CUDA_TRY(cudaFree(c->lsh_scratch));
-      c->lsh_scratch = nullptr;
-      c->lsh_scratch_bytes = 0;
-      CUDA_TRY(cudaMalloc(&c->lsh_scratch, need));
-      c->lsh_scratch_bytes = need;
+    slot = (int)(c->lsh_next++ % dsk_ctx::kLshSlots);
+    if (!c->lsh_last[slot])
+      CUDA_TRY(cudaEventCreateWithFlags(&c->lsh_last[slot], cudaEventDisableTiming));
+    else
+      CUDA_TRY(cudaStreamWaitEvent(st, c->lsh_last[slot], 0));
+    if (c->lsh_scratch_bytes[slot] < need) {
+      CUDA_TRY(cudaEventSynchronize(c->lsh_last[slot]));
+      if (c->lsh_scratch[slot]) CUDA_TRY(cudaFree(c->lsh_scratch[slot]));
+      c->lsh_scratch[slot] = nullptr;
+      c->lsh_scratch_bytes[slot] = 0;
+      CUDA_TRY(cudaMalloc(&c->lsh_scratch[slot], need));
+      c->lsh_scratch_bytes[slot] = need;
     }
+    scratch = c->lsh_scratch[slot];
   }
   unsigned long long *counter = c->d_counter + (c->next_slot.fetch_add(1) % kCounterSlots);
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
@@ -40,7 +52,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.exact_sort = ex && atoi(ex) != 0; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
   a.md = make_mod((uint32_t)L); a.G = G; a.out_keys = out_keys; a.out_fps = out_fps;
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
-  a.scratch = (unsigned char *)c->lsh_scratch; a.team_scratch = team_bytes; a.cap = cap;
+  a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap;
   a.tabs = table_args(c, (double)t);
   switch (NW) {
     case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
@@ -48,6 +60,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
   }
   CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaEventRecord(c->lsh_last[slot], st));
   return DSK_OK;
 }
 
@@ -97,5 +110,5 @@ extern "C" int dsk_lsh_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_
       CUDA_TRY(cudaMemcpyAsync(stats + r0 * 4, dst + r0 * 4, m * 16, cudaMemcpyDeviceToHost, st));
     return DSK_OK;
   };
-  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, 1, launch, out);  // shared scratch
+  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, 2, launch, out);
 }

@@ -369,6 +369,25 @@ def test_lsh_sort_paths_agree(monkeypatch, scale_exp):
     assert np.array_equal(as_u64(fast.fps), fps)
 
 
+def test_lsh_concurrent_streams():
+    """LSH launches on different streams take separate hit-buffer slots."""
+    parts = [workloads.generate("cfg4", n=3000, start=s0) for s0 in (0, 3000, 6000, 9000, 12000)]
+    f = fam(3)
+    serial = [as_u64(lsh_batch(*p, LshParams(100, 20), f).keys) for p in parts]
+    dev = torch.device("cuda", 0)
+    ins = [tuple(torch.from_numpy(np.asarray(a).view(np.int64) if a.dtype == np.uint64 else a)
+                 .to(dev) for a in p) for p in parts]
+    streams = [torch.cuda.Stream(dev) for _ in parts]
+    torch.cuda.synchronize()
+    outs = []
+    for st, p in zip(streams, ins):
+        with torch.cuda.stream(st):
+            outs.append(lsh_batch(*p, LshParams(100, 20), f, check=False))
+    torch.cuda.synchronize()
+    for o, ref in zip(outs, serial):
+        assert np.array_equal(as_u64(o.keys), ref)
+
+
 def test_lsh_cfg4_vs_oracle():
     indptr, ids, w = workloads.generate("cfg4", n=400, start=5000)
     f = fam(3)
