@@ -751,23 +751,35 @@ static TableArgs table_args(const dsk_ctx *c, double tf) {
 // named barriers 1..15
 static bool team_size_ok(int G, int nw) { return nw % G == 0 && (G == 1 || nw / G <= 15); }
 
-// (CTA width, team size): the smallest team whose slot arrays fit beside the
-// queues, preferring the wider CTA on ties
+// (CTA width, team size).  Large batches: the smallest team whose slot
+// arrays fit beside the queues (most teams in flight), preferring the wider
+// CTA on ties.  Batches that fit in one wave of teams (n <= SMs * teams, e.g.
+// single-set calls): the largest team that still gives every set its own
+// team, so the warps of a CTA share few sets and each set finishes sooner.
 template <class SmemFn>
-static bool choose_shape(const dsk_ctx *c, SmemFn smem_of, int &nw_out, int &g_out) {
-  int best_g = 1 << 30, best_nw = 0;
+static bool choose_shape(const dsk_ctx *c, SmemFn smem_of, int64_t n, int &nw_out,
+                         int &g_out) {
+  int best_g = 1 << 30, best_nw = 0;       // large-batch rule
+  int wave_g = 0, wave_nw = 0;             // one-wave rule
   const char *force = getenv("DSK_NW");  // tuning: restrict to one CTA width
   for (int nw : kWidths) {
     if (force && atoi(force) != nw) continue;
+    int gmin = 0;
     for (int G = 1; G <= nw; G++) {
       if (!team_size_ok(G, nw) || smem_of(G, nw) > c->max_smem) continue;
-      if (G < best_g) { best_g = G; best_nw = nw; }
-      break;
+      if (!gmin) gmin = G;
+      if ((int64_t)c->num_sms * (nw / G) >= n && G > wave_g) { wave_g = G; wave_nw = nw; }
     }
+    if (gmin && gmin < best_g) { best_g = gmin; best_nw = nw; }
   }
   if (!best_nw) return false;
-  nw_out = best_nw;
-  g_out = best_g;
+  if (wave_nw && !getenv("DSK_NO_WAVE")) {
+    nw_out = wave_nw;
+    g_out = wave_g;
+  } else {
+    nw_out = best_nw;
+    g_out = best_g;
+  }
   return true;
 }
 
@@ -781,7 +793,7 @@ extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
   int64_t t = dsk_minhash_density(k);
   if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "k too large");
   int NW = 0, G = 0;
-  if (!choose_shape(c, [&](int g, int nw) { return minhash_smem(k, g, nw); }, NW, G))
+  if (!choose_shape(c, [&](int g, int nw) { return minhash_smem(k, g, nw); }, n, NW, G))
     return set_err(DSK_EUNSUPPORTED, "k too large for the shared-memory slot array");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
