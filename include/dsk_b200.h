@@ -39,7 +39,7 @@ extern "C" {
 #define DSK_NOCONV 5   /* RuntimeError: buckets unfilled after 64 steps  ref/sketching.py:112 */
 #define DSK_LIMIT 6    /* ValidationError rank limit <= 0 or infinite    ref/darthash.py:136-138 */
 #define DSK_SCRATCH 7  /* LSH hit buffer overflow (library limit, not a reference error) */
-#define DSK_TOOLARGE 8 /* dsk_darts_csr: set has >= 4096 elements (library limit) */
+#define DSK_TOOLARGE 8 /* reserved (no longer returned: large sets are enumerated in slices) */
 #define DSK_STATUS_TIE 0x100
 
 /* call-level error codes */

@@ -41,7 +41,7 @@ _STATUS_ERRORS = {
     DSK_NOCONV: (RuntimeError, "bucket filling did not converge; hash family is broken"),
     DSK_LIMIT: (ValidationError, "rank limit must be positive and finite"),
     7: (RuntimeError, "LSH hit buffer overflow (library limit)"),
-    8: (RuntimeError, "set too large for dart materialisation (>= 4096 elements)"),
+    8: (RuntimeError, "set too large (reserved status)"),
 }
 
 

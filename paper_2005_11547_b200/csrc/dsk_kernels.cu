@@ -467,6 +467,8 @@ struct DartsArgs {
   TableArgs tabs;
 };
 
+constexpr int64_t kSliceElems = 4096;  // element index field of the row sink (12 bits)
+
 struct RowSink {
   static constexpr bool kFuse = true;
   const DartsArgs *a;
@@ -513,7 +515,6 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
     const double L = a.rank_limit[s];
     int status = 0;
     if (nnz == 0) status = DSK_EMPTY;                           // ref/darthash.py:133-134
-    else if (nnz >= 4096) status = DSK_TOOLARGE;  // element index field of the row sink
     else if (!(L > 0.0) || isinf(L)) status = DSK_LIMIT;        // :136-138
     int maxd = 0;
     for (int64_t i = lane; i < nnz && status == 0; i += 32) {
@@ -536,29 +537,37 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
       P.RD_lo = 0;
       P.maxd = maxd;
       poisson_regs(P, T);
-      RowSink sink;
-      sink.a = &a;
-      sink.set = s;
-      sink.lo = lo;
-      sink.cursor = &cursors[warp];
-      // the area cap is checked on a counting pass first (ref/darthash.py:242-244
-      // raises before any dart is produced)
       if (lane == 0) pps[warp] = P;
       __syncwarp();
-      Engine<RowSink, true> eng(T, Q, rwin, sink, pps[warp], lane);
-      int64_t next = 0;
-      eng.run([&](bool &valid, uint64_t &id, double &x, int &depth, uint32_t &eidx) -> bool {
-        int64_t c = next++;
-        if (c * 32 >= nnz) return false;
-        int64_t e = c * 32 + lane;
-        valid = e < nnz;
-        id = valid ? a.ids[lo + e] : 0;
-        x = valid ? a.w[lo + e] : 0.0;
-        depth = valid ? floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, x)), T.l2thr) : 0;
-        eidx = (uint32_t)e;
-        return true;
-      });
-      if (eng.abort) status = DSK_AREAS;
+      // the row sink carries a 12-bit element index, so large sets are
+      // enumerated in slices of 4096 elements (darts of an element depend on
+      // that element alone); the area cap applies to the whole set
+      // (ref/darthash.py:242-244; dsk_darts_csr runs a counting pass first,
+      // so a capped set produces no rows)
+      double full = 0.0;
+      for (int64_t base = 0; base < nnz && status == 0; base += kSliceElems) {
+        const int64_t m = nnz - base < kSliceElems ? nnz - base : kSliceElems;
+        RowSink sink;
+        sink.a = &a;
+        sink.set = s;
+        sink.lo = lo + base;
+        sink.cursor = &cursors[warp];
+        Engine<RowSink, true> eng(T, Q, rwin, sink, pps[warp], lane);
+        int64_t next = 0;
+        eng.run([&](bool &valid, uint64_t &id, double &x, int &depth, uint32_t &eidx) -> bool {
+          int64_t c = next++;
+          if (c * 32 >= m) return false;
+          int64_t e = c * 32 + lane;
+          valid = e < m;
+          id = valid ? a.ids[lo + base + e] : 0;
+          x = valid ? a.w[lo + base + e] : 0.0;
+          depth = valid ? floor_log2_host(__dadd_rn(1.0, __dmul_rn(a.tf, x)), T.l2thr) : 0;
+          eidx = (uint32_t)e;
+          return true;
+        });
+        full += eng.warp_full();
+        if (eng.abort || full > kMaxAreas) status = DSK_AREAS;
+      }
     }
     __syncwarp();
     if (lane == 0) {

@@ -580,6 +580,52 @@ def test_bottom_k_single_set_api_and_oracle():
         assert st == 0 and np.array_equal(fp[s], od["fingerprint"])
 
 
+def _dart_rows(offsets, cols, q):
+    off = offsets.cpu().numpy()
+    a, b = off[q], off[q + 1]
+    arr = np.empty(b - a, dtype=[("element", "<u8"), ("nu", "<u2"), ("rho", "<u2"),
+                                 ("w", "<u4"), ("r", "<u4"), ("j", "<u2"),
+                                 ("weight", "<f8"), ("rank", "<f8"), ("fingerprint", "<u8")])
+    for name in arr.dtype.names:
+        v = cols[name][a:b].cpu().numpy()
+        arr[name] = v.view(arr.dtype[name]) if v.dtype.itemsize == arr.dtype[name].itemsize \
+            else v
+    return arr
+
+
+def test_darts_and_bottom_k_large_sets_vs_oracle():
+    """Sets beyond the row sink's 4096-element slice: enumerated slice by
+    slice, darts tuple-for-tuple and bottom-k identical to the oracle."""
+    lens = [4095, 4096, 4097, 9000, 1, 20000]
+    indptr, ids, w = _ragged_batch(31, lens, sigma=1.5)
+    f = fam(0x31)
+    orc = Oracle(0x31)
+    limits = np.array([1.0 / float(np.sum(w[indptr[s]:indptr[s + 1]])) for s in range(len(lens))])
+    offsets, status, cols = darts_batch(indptr, ids, w, 64, limits, f)
+    assert (status.cpu().numpy() == 0).all()
+    for s in range(len(lens)):
+        st, od = orc.darts_below_rank(ids[indptr[s]:indptr[s + 1]], w[indptr[s]:indptr[s + 1]],
+                                      64, float(limits[s]))
+        assert st == 0
+        got = canonical_darts(_dart_rows(offsets, cols, s))
+        assert np.array_equal(got, canonical_darts(od)), s
+    # area cap over the whole set (ref/darthash.py:242-244) when no single
+    # lane's share exceeds it: 20000 elements, ~2.5e8 areas in total
+    cid = np.arange(20000, dtype=np.uint64) * 7 + 3
+    cw = np.ones(20000)
+    _, cst, _ = darts_batch(np.array([0, 20000]), cid, cw, 64, np.array([100.0]), f)
+    assert cst.cpu().numpy()[0] == 4 == orc.darts_below_rank(cid, cw, 64, 100.0)[0]
+    from paper_2005_11547_b200 import bottom_k_batch
+    res = bottom_k_batch(indptr, ids, w, 50, f)
+    fp = as_u64(res.columns["fingerprint"])
+    rk = res.columns["rank"].cpu().numpy()
+    for s in range(len(lens)):
+        st, phi, od = orc.bottom_k(ids[indptr[s]:indptr[s + 1]], w[indptr[s]:indptr[s + 1]], 50)
+        assert st == 0
+        assert np.array_equal(fp[s], od["fingerprint"]), s
+        assert np.array_equal(rk[s], od["rank"]), s
+
+
 def test_dsk1_records_byte_identical():
     from paper_2005_11547_b200 import (BottomKFingerprints, MinHashSketch, bottom_k_batch,
                                        dump_sketches, iter_sketches)
