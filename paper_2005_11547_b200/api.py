@@ -729,7 +729,10 @@ def dump_sketches(payload: torch.Tensor, kind: int, k: int, seed: int) -> bytes:
         _lib.check(_lib.load().dsk_dsk1_records(int(kind), int(k), int(seed) & (2**64 - 1),
                                                 _ptr(payload.contiguous()), n, _ptr(out),
                                                 _stream_ptr(dev)), "dsk_dsk1_records")
-    return out.cpu().numpy().tobytes()
+    host = torch.empty(out.numel(), dtype=torch.uint8, pin_memory=True)
+    host.copy_(out, non_blocking=True)
+    torch.cuda.current_stream(dev).synchronize()
+    return host.numpy().tobytes()
 
 
 def dump_sketch(sketch) -> bytes:

@@ -56,6 +56,26 @@ __global__ void dsk1_kernel(int kind, uint32_t k, uint64_t seed, const uint64_t 
   }
 }
 
+// Records whose size is a multiple of 4 bytes (every kind 1 / 3 record, and
+// kind 2 when ceil(k/8) % 4 == 0): one warp per record writes it as aligned
+// 32-bit words -- 5 header words, then the little-endian payload -- so the
+// stores coalesce and no per-byte index arithmetic is needed (HBM-bound).
+__global__ void dsk1_words_kernel(int kind, uint32_t k, uint64_t seed, const uint64_t *payload,
+                                  int64_t words_per_set, int64_t payload_bytes, int64_t n,
+                                  uint32_t *out) {
+  const int64_t rw = (20 + payload_bytes) / 4;  // 32-bit words per record
+  const int lane = threadIdx.x & 31;
+  const uint32_t hdr[5] = {0x314b5344u /* "DSK1" */,
+                           1u | ((uint32_t)kind << 8),  // version 1, kind, reserved 0
+                           k, (uint32_t)seed, (uint32_t)(seed >> 32)};
+  for (int64_t s = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; s < n;
+       s += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+    uint32_t *o = out + s * rw;
+    const uint32_t *pl = reinterpret_cast<const uint32_t *>(payload + s * words_per_set);
+    for (int64_t q = lane; q < rw; q += 32) o[q] = q < 5 ? hdr[q] : pl[q - 5];
+  }
+}
+
 // kind 1 (minhash) and 3 (bottom-k): payload = k uint64 values per set;
 // kind 2 (one-bit): payload = ceil(k/8) bytes of the packed words
 // (np.packbits(bits, bitorder="little"), ref/sketching.py:229).
@@ -67,6 +87,14 @@ extern "C" int dsk_dsk1_records(int32_t kind, int32_t k, uint64_t seed, const ui
   const int64_t words = kind == 2 ? (k + 63) / 64 : k;
   const int64_t pbytes = kind == 2 ? (k + 7) / 8 : 8 * (int64_t)k;
   int64_t total = n * (20 + pbytes);
+  if ((pbytes & 3) == 0 && ((uintptr_t)out & 3) == 0) {
+    int64_t wgrid = (n + 7) / 8;  // 8 warps per block
+    int grid = (int)(wgrid < 148 * 64 ? wgrid : 148 * 64);
+    dsk1_words_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+        kind, (uint32_t)k, seed, payload, words, pbytes, n, reinterpret_cast<uint32_t *>(out));
+    CUDA_TRY(cudaGetLastError());
+    return DSK_OK;
+  }
   int grid = (int)((total + 255) / 256);
   if (grid > 148 * 32) grid = 148 * 32;
   dsk1_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(kind, (uint32_t)k, seed, payload, words,

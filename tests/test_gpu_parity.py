@@ -640,6 +640,14 @@ def test_dsk1_records_byte_identical():
     assert isinstance(recs[0], MinHashSketch)
     assert np.array_equal(np.stack([r.values for r in recs]), as_u64(res.values))
     assert isinstance(list(iter_sketches(g["dsk1_bottomk"].tobytes()))[0], BottomKFingerprints)
+    # word-aligned one-bit records (k = 256: 32-byte payload) against
+    # struct.pack + np.packbits as ref/sketching.py:224-231 writes them
+    import struct
+    r2 = minhash_batch(g["indptr"], g["ids"], g["w"], 256, f, bits=True)
+    bits = (as_u64(r2.values) & np.uint64(1)).astype(np.uint8)
+    exp = b"".join(struct.pack("<4sBBHIQ", b"DSK1", 1, 2, 0, 256, f.seed) +
+                   np.packbits(row, bitorder="little").tobytes() for row in bits)
+    assert dump_sketches(r2.bits, 2, 256, f.seed) == exp
 
 
 # ------------------------------------------------------- LshIndex (next row)
