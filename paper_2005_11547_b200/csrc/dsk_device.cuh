@@ -276,4 +276,25 @@ __device__ __forceinline__ void ld128_shared(const uint64_t *addr, uint64_t &lo,
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(a) : "memory");
 }
 
+// generic-address forms (slot arrays in global memory for large k)
+__device__ __forceinline__ void cas128_generic(uint64_t *addr, uint64_t cmp_lo, uint64_t cmp_hi,
+                                               uint64_t val_lo, uint64_t val_hi, uint64_t &old_lo,
+                                               uint64_t &old_hi) {
+  asm volatile(
+      "{\n\t.reg .b128 c, v, o;\n\t"
+      "mov.b128 c, {%2, %3};\n\t"
+      "mov.b128 v, {%4, %5};\n\t"
+      "atom.cas.b128 o, [%6], c, v;\n\t"
+      "mov.b128 {%0, %1}, o;\n\t}"
+      : "=l"(old_lo), "=l"(old_hi)
+      : "l"(cmp_lo), "l"(cmp_hi), "l"(val_lo), "l"(val_hi), "l"(addr)
+      : "memory");
+}
+
+// a stale (older) pair is harmless: slot values only decrease, and a failed
+// CAS returns the current pair
+__device__ __forceinline__ void ld128_generic(const uint64_t *addr, uint64_t &lo, uint64_t &hi) {
+  asm volatile("ld.relaxed.gpu.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "l"(addr) : "memory");
+}
+
 }  // namespace dsk

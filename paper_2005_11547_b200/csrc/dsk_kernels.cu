@@ -47,14 +47,15 @@ struct dsk_ctx {
   size_t stage_bytes = 0;
   cudaStream_t hs[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in[kMaxChunks] = {}, ev_k[kMaxChunks] = {};
-  // LSH hit buffers (one slice per resident team), a small pool of slots
-  // reused in stream order: a launch waits for the previous user of its slot
+  // global scratch of the kernels (LSH hit buffers, large-k minhash slot
+  // arrays): a small pool of slots reused in stream order, a launch waits for
+  // the previous user of its slot (scratch_acquire / scratch_release)
   std::mutex scratch_mu;
-  static constexpr int kLshSlots = 4;
-  void *lsh_scratch[kLshSlots] = {};
-  size_t lsh_scratch_bytes[kLshSlots] = {};
-  cudaEvent_t lsh_last[kLshSlots] = {};
-  unsigned lsh_next = 0;
+  static constexpr int kScratchSlots = 4;
+  void *scratch[kScratchSlots] = {};
+  size_t scratch_bytes[kScratchSlots] = {};
+  cudaEvent_t scratch_last[kScratchSlots] = {};
+  unsigned scratch_next = 0;
 };
 
 constexpr int kCounterSlots = 256;
@@ -163,6 +164,7 @@ __device__ __forceinline__ void team_sync(int G, int team) {
 
 // ------------------------------------------------------------- minhash
 
+template <bool kGlobal>  // slots in global memory (k too large for shared memory)
 struct MinhashSink {
   static constexpr bool kFuse = true;
   uint64_t *slots;  // 2*k words: {rank bits, fingerprint} per slot, 16-B aligned
@@ -182,7 +184,8 @@ struct MinhashSink {
       uint64_t *sl = slots + 2 * (size_t)b;
       uint64_t rb = (uint64_t)__double_as_longlong(h.rank);
       uint64_t cr, cf;
-      ld128_shared(sl, cr, cf);
+      if (kGlobal) ld128_generic(sl, cr, cf);
+      else ld128_shared(sl, cr, cf);
       while (true) {
         if (rb > cr || (rb == cr && h.fp >= cf)) {
           if (rb == cr && h.fp != cf) t = true;
@@ -190,7 +193,8 @@ struct MinhashSink {
         }
         if (rb == cr) t = true;
         uint64_t orr, off;
-        cas128_shared(sl, cr, cf, rb, h.fp, orr, off);
+        if (kGlobal) cas128_generic(sl, cr, cf, rb, h.fp, orr, off);
+        else cas128_shared(sl, cr, cf, rb, h.fp, orr, off);
         if (orr == cr && off == cf) {
           if (cr == kEmptyRank) newly = 1;
           break;
@@ -225,6 +229,7 @@ struct MinhashArgs {
   int32_t *phi;
   uint32_t *stats;
   unsigned long long *counter;
+  uint64_t *gslots;  // non-null: slot arrays in global memory, 2*k words per team
   TableArgs tabs;
 };
 
@@ -321,7 +326,7 @@ __device__ __forceinline__ void poisson_regs(PassParams &P, const SmemTables &T)
   P.pt3 = T.pthr[3];
 }
 
-template <int NW>
+template <int NW, bool kGlobal = false>
 __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
@@ -332,11 +337,13 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
   TeamCtl &C = *reinterpret_cast<TeamCtl *>(smem + off_team(NW) + team * kTeamCtlBytes);
   const int teams = NW / G;
-  uint64_t *slots = reinterpret_cast<uint64_t *>(smem + off_team(NW) + teams * kTeamCtlBytes) +
+  uint64_t *slots =
+      kGlobal ? a.gslots + ((size_t)blockIdx.x * teams + team) * 2 * (size_t)k
+              : reinterpret_cast<uint64_t *>(smem + off_team(NW) + teams * kTeamCtlBytes) +
                     (size_t)team * 2 * k;
   __syncthreads();
 
-  MinhashSink sink;
+  MinhashSink<kGlobal> sink;
   sink.slots = slots;
   sink.md = a.md;
   sink.filled = &C.filled;
@@ -676,9 +683,9 @@ __global__ void __launch_bounds__(512) hash_peak_kernel(const uint64_t *tab, int
 
 // ------------------------------------------------------------- host side
 
-static size_t minhash_smem(int k, int G, int nw) {
+static size_t minhash_smem(int k, int G, int nw, bool global_slots = false) {
   int teams = nw / G;
-  return off_team(nw) + teams * kTeamCtlBytes + (size_t)teams * k * 16;
+  return off_team(nw) + teams * kTeamCtlBytes + (global_slots ? 0 : (size_t)teams * k * 16);
 }
 
 extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const double *cdf_host,
@@ -711,6 +718,8 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<20, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(darts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -731,9 +740,9 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
   cudaFree(c->d_l2thr);
   cudaFree(c->d_counter);
   if (c->stage) cudaFree(c->stage);
-  for (int i = 0; i < dsk_ctx::kLshSlots; i++) {
-    if (c->lsh_scratch[i]) cudaFree(c->lsh_scratch[i]);
-    if (c->lsh_last[i]) cudaEventDestroy(c->lsh_last[i]);
+  for (int i = 0; i < dsk_ctx::kScratchSlots; i++) {
+    if (c->scratch[i]) cudaFree(c->scratch[i]);
+    if (c->scratch_last[i]) cudaEventDestroy(c->scratch_last[i]);
   }
   for (int i = 0; i < 4; i++)
     if (c->hs[i]) cudaStreamDestroy(c->hs[i]);
@@ -792,6 +801,32 @@ static bool choose_shape(const dsk_ctx *c, SmemFn smem_of, int64_t n, int &nw_ou
   return true;
 }
 
+// Stream-ordered scratch: the caller holds c->scratch_mu from acquire until
+// release (after its launch), so concurrent calls on different streams never
+// share a buffer and a reused slot waits for its previous launch.
+static int scratch_acquire(dsk_ctx *c, size_t need, cudaStream_t st, int &slot, void *&ptr) {
+  slot = (int)(c->scratch_next++ % dsk_ctx::kScratchSlots);
+  if (!c->scratch_last[slot])
+    CUDA_TRY(cudaEventCreateWithFlags(&c->scratch_last[slot], cudaEventDisableTiming));
+  else
+    CUDA_TRY(cudaStreamWaitEvent(st, c->scratch_last[slot], 0));
+  if (c->scratch_bytes[slot] < need) {
+    CUDA_TRY(cudaEventSynchronize(c->scratch_last[slot]));
+    if (c->scratch[slot]) CUDA_TRY(cudaFree(c->scratch[slot]));
+    c->scratch[slot] = nullptr;
+    c->scratch_bytes[slot] = 0;
+    CUDA_TRY(cudaMalloc(&c->scratch[slot], need));
+    c->scratch_bytes[slot] = need;
+  }
+  ptr = c->scratch[slot];
+  return DSK_OK;
+}
+
+static int scratch_release(dsk_ctx *c, int slot, cudaStream_t st) {
+  CUDA_TRY(cudaEventRecord(c->scratch_last[slot], st));
+  return DSK_OK;
+}
+
 extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                                const double *weights, int64_t n, int32_t k, uint64_t *out_values,
                                uint64_t *out_bits, int32_t *status, int32_t *phi, uint32_t *stats,
@@ -802,8 +837,14 @@ extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
   int64_t t = dsk_minhash_density(k);
   if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "k too large");
   int NW = 0, G = 0;
-  if (!choose_shape(c, [&](int g, int nw) { return minhash_smem(k, g, nw); }, n, NW, G))
-    return set_err(DSK_EUNSUPPORTED, "k too large for the shared-memory slot array");
+  // slot arrays in shared memory; k too large for that -> global memory (L2)
+  bool global_slots = false;
+  if (!choose_shape(c, [&](int g, int nw) { return minhash_smem(k, g, nw); }, n, NW, G)) {
+    global_slots = true;  // (instantiated for the 20-warp CTA only)
+    if (!choose_shape(c, [&](int g, int nw) {
+          return nw == 20 ? minhash_smem(k, g, nw, true) : (size_t)1 << 40; }, n, NW, G))
+      return set_err(DSK_EUNSUPPORTED, "no CTA shape fits shared memory");
+  }
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
   // each launch owns one counter slot; slots recycle after kCounterSlots launches,
@@ -815,15 +856,30 @@ extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
   a.tf = (double)t; a.inv_t = 1.0 / (double)t; a.md = make_mod((uint32_t)k); a.G = G;
   a.out_values = out_values; a.out_bits = out_bits; a.status = status; a.phi = phi;
   a.stats = stats; a.counter = counter; a.tabs = table_args(c, (double)t);
-  size_t smem = minhash_smem(k, G, NW);
+  a.gslots = nullptr;
+  size_t smem = minhash_smem(k, G, NW, global_slots);
   int grid = c->num_sms;
   if ((int64_t)grid * (NW / G) > n) grid = (int)((n + (NW / G) - 1) / (NW / G));
-  switch (NW) {
-    case 24: minhash_kernel<24><<<grid, 24 * 32, smem, st>>>(a); break;
-    case 22: minhash_kernel<22><<<grid, 22 * 32, smem, st>>>(a); break;
-    default: minhash_kernel<20><<<grid, 20 * 32, smem, st>>>(a); break;
+  std::unique_lock<std::mutex> lock(c->scratch_mu, std::defer_lock);
+  int slot = -1;
+  if (global_slots) {
+    lock.lock();
+    void *p = nullptr;
+    int rc = scratch_acquire(c, (size_t)grid * (NW / G) * 16 * (size_t)k, st, slot, p);
+    if (rc) return rc;
+    a.gslots = (uint64_t *)p;
+  }
+  if (global_slots) {
+    minhash_kernel<20, true><<<grid, 20 * 32, smem, st>>>(a);
+  } else {
+    switch (NW) {
+      case 24: minhash_kernel<24><<<grid, 24 * 32, smem, st>>>(a); break;
+      case 22: minhash_kernel<22><<<grid, 22 * 32, smem, st>>>(a); break;
+      default: minhash_kernel<20><<<grid, 20 * 32, smem, st>>>(a); break;
+    }
   }
   CUDA_TRY(cudaGetLastError());
+  if (slot >= 0) return scratch_release(c, slot, st);
   return DSK_OK;
 }
 

@@ -21,27 +21,13 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   uint32_t cap = (uint32_t)(8 * t > 16384 ? 8 * t : 16384);
   size_t team_bytes = align16((size_t)cap * 24) + align16((size_t)L * K * 8);
   size_t need = (size_t)grid * teams * team_bytes;
-  // scratch slot: stream-ordered reuse (waits for the slot's previous launch),
-  // so concurrent calls on different streams never share a hit buffer
-  // (the lock is held until the slot's event is recorded after the launch)
+  // hit buffers from the context's stream-ordered scratch pool
   std::lock_guard<std::mutex> lock(c->scratch_mu);
   int slot;
   void *scratch;
   {
-    slot = (int)(c->lsh_next++ % dsk_ctx::kLshSlots);
-    if (!c->lsh_last[slot])
-      CUDA_TRY(cudaEventCreateWithFlags(&c->lsh_last[slot], cudaEventDisableTiming));
-    else
-      CUDA_TRY(cudaStreamWaitEvent(st, c->lsh_last[slot], 0));
-    if (c->lsh_scratch_bytes[slot] < need) {
-      CUDA_TRY(cudaEventSynchronize(c->lsh_last[slot]));
-      if (c->lsh_scratch[slot]) CUDA_TRY(cudaFree(c->lsh_scratch[slot]));
-      c->lsh_scratch[slot] = nullptr;
-      c->lsh_scratch_bytes[slot] = 0;
-      CUDA_TRY(cudaMalloc(&c->lsh_scratch[slot], need));
-      c->lsh_scratch_bytes[slot] = need;
-    }
-    scratch = c->lsh_scratch[slot];
+    int rc = scratch_acquire(c, need, st, slot, scratch);
+    if (rc) return rc;
   }
   unsigned long long *counter = c->d_counter + (c->next_slot.fetch_add(1) % kCounterSlots);
   CUDA_TRY(cudaMemsetAsync(counter, 0, sizeof(unsigned long long), st));
@@ -60,8 +46,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
   }
   CUDA_TRY(cudaGetLastError());
-  CUDA_TRY(cudaEventRecord(c->lsh_last[slot], st));
-  return DSK_OK;
+  return scratch_release(c, slot, st);
 }
 
 extern "C" int dsk_lsh_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,

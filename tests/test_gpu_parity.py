@@ -216,6 +216,22 @@ def test_minhash_max_sizes_and_ragged_vs_oracle():
         assert np.array_equal(got_h[ok], hits[ok]), k
 
 
+@pytest.mark.parametrize("k", [5000, 12000])
+def test_minhash_large_k_global_slots_vs_oracle(k):
+    """k beyond the shared-memory slot array: slots live in global memory."""
+    indptr, ids, w = workloads.generate("cfg1", n=6)
+    res = minhash_batch(indptr, ids, w, k, fam(0), bits=True)
+    vals, status, phi, hits = Oracle(0).minhash_csr(indptr, ids, w, k)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(res.values), vals)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+    assert np.array_equal(res.stats.cpu().numpy().view(np.uint32)[:, 2].astype(np.int64), hits)
+    packed = np.packbits((vals & np.uint64(1)).astype(np.uint8), axis=1, bitorder="little")
+    pad = np.zeros((6, ((k + 63) // 64) * 8), dtype=np.uint8)
+    pad[:, :packed.shape[1]] = packed
+    assert np.array_equal(as_u64(res.bits), pad.view("<u8"))
+
+
 def test_lsh_max_sizes_vs_oracle():
     lens = [16384, 1, 4000, 16384, 2, 20000]
     indptr, ids, w = _ragged_batch(22, lens, sigma=1.0)
