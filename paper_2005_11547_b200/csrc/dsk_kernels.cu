@@ -26,6 +26,10 @@
 #include "dsk_device.cuh"
 #include "dsk_engine.cuh"
 
+#ifndef DSK_OPAQUE
+#define DSK_OPAQUE 1
+#endif
+
 using namespace dsk;
 
 // ------------------------------------------------------------- context
@@ -326,13 +330,30 @@ __device__ __forceinline__ void poisson_regs(PassParams &P, const SmemTables &T)
   P.pt3 = T.pthr[3];
 }
 
+// Thread coordinates the compiler cannot rematerialise from special
+// registers (at 80 registers it otherwise re-derives them, S2R included, at
+// many uses); it keeps or spills them instead.
+__device__ __forceinline__ int opaque_int(int v) {
+#if DSK_OPAQUE
+  asm volatile("" : "+r"(v));
+#endif
+  return v;
+}
+__device__ __forceinline__ int opaque_team(int v) {
+#if DSK_OPAQUE >= 2
+  asm volatile("" : "+r"(v));
+#endif
+  return v;
+}
+
 template <int NW, bool kGlobal = false>
 __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
   load_tables(T, a.tabs);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = a.G, team = warp / G, wit = warp % G, tt = wit * 32 + lane;
+  const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
+  const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
+            tt = opaque_team(wit * 32 + lane);
   const int k = a.k;
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
   TeamCtl &C = *reinterpret_cast<TeamCtl *>(smem + off_team(NW) + team * kTeamCtlBytes);
@@ -506,7 +527,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
   load_tables(T, a.tabs);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
   unsigned long long *cursors =
       reinterpret_cast<unsigned long long *>(smem + kOffTeam);

@@ -92,8 +92,9 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
   load_tables(T, a.tabs);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = a.G, team = warp / G, wit = warp % G, tt = wit * 32 + lane;
+  const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
+  const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
+            tt = opaque_team(wit * 32 + lane);
   const int L = a.L, K = a.K;
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
   unsigned char *tb = smem + off_team(NW) + team * lsh_team_bytes(L);
