@@ -15,9 +15,7 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "op1": {"DSK_OPAQUE": 1},
-    "op2": {"DSK_OPAQUE": 2},
-    "op0": {"DSK_OPAQUE": 0},
+    "kd": {},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
