@@ -75,3 +75,64 @@ def sharded_minhash(indptr, ids, weights, k: int, hashes, *, bits: bool = False,
     if gather and world > 1:
         return bounds, res, gather_rows(res.values, bounds, group)
     return bounds, res
+
+
+def minhash_host_multi(indptr, ids, weights, k: int, hashes, *, devices=None, bits: bool = False,
+                       check: bool = True):
+    """dart_minhash for a CSR batch in host memory, row-sharded over several
+    GPUs driven by this one process.
+
+    Each device sketches a contiguous, work-balanced row range through the
+    host-buffer C entry point (dsk_minhash_csr_host: chunked copy-in /
+    sketch / copy-out pipeline) and writes its rows straight into disjoint
+    slices of the host outputs -- the "host gather", no collective.  One host
+    thread per device (ctypes releases the GIL for the call).  Pinned input
+    arrays give full PCIe overlap.
+
+    Returns (values uint64[n, k], bits uint64[n, ceil(k/64)] or None,
+    status int32[n]) as numpy arrays.
+    """
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import _lib
+    from .api import raise_for_status
+    from .constants import ValidationError, minhash_density
+    if k < 1:
+        raise ValidationError(f"k must be positive, got {k}")
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    weights = np.ascontiguousarray(weights, dtype=np.float64)
+    n = indptr.size - 1
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = [int(d) for d in devices]
+    words = (k + 63) // 64
+    values = np.zeros((n, k), dtype=np.uint64)
+    packed = np.zeros((n, words), dtype=np.uint64) if bits else None
+    status = np.zeros(n, dtype=np.int32)
+    bounds = plan_shards(indptr, len(devices), minhash_density(k))
+    ctxs = [hashes.context(torch.device("cuda", d)) for d in devices]  # created up front
+    lib = _lib.load()
+    P = ctypes.c_void_p
+
+    def run(r):
+        r0, r1 = int(bounds[r]), int(bounds[r + 1])
+        if r1 == r0:
+            return 0
+        e0 = int(indptr[r0])
+        local = np.ascontiguousarray(indptr[r0:r1 + 1] - e0)
+        with torch.cuda.device(devices[r]):
+            return lib.dsk_minhash_csr_host(
+                ctxs[r], P(local.ctypes.data), P(ids.ctypes.data + 8 * e0),
+                P(weights.ctypes.data + 8 * e0), r1 - r0, k, P(values.ctypes.data + 8 * k * r0),
+                P(packed.ctypes.data + 8 * words * r0) if bits else None,
+                P(status.ctypes.data + 4 * r0), None, None)
+
+    with ThreadPoolExecutor(max_workers=len(devices)) as pool:
+        rcs = list(pool.map(run, range(len(devices))))
+    for rc in rcs:
+        _lib.check(rc, "dsk_minhash_csr_host")
+    if check:
+        raise_for_status(torch.from_numpy(status))
+    return values, packed, status

@@ -385,6 +385,21 @@ def test_lsh_sort_paths_agree(monkeypatch, scale_exp):
     assert np.array_equal(as_u64(fast.fps), fps)
 
 
+def test_minhash_host_multi_device_gather():
+    """Single-process multi-GPU host path: row shards through
+    dsk_minhash_csr_host written into disjoint slices of the host outputs.
+    Three shards on device 0 stand in for three GPUs (same partition logic)."""
+    from paper_2005_11547_b200.shard import minhash_host_multi
+    indptr, ids, w = workloads.generate("cfg2", n=2000, start=100)
+    f = fam(1)
+    dev = minhash_batch(indptr, ids, w, 256, f, bits=True)
+    for devices in ([0], [0, 0, 0]):
+        vals, bits, status = minhash_host_multi(indptr, ids, w, 256, f, devices=devices, bits=True)
+        assert (status == 0).all()
+        assert np.array_equal(vals, as_u64(dev.values))
+        assert np.array_equal(bits, as_u64(dev.bits))
+
+
 def test_lsh_concurrent_streams():
     """LSH launches on different streams take separate hit-buffer slots."""
     parts = [workloads.generate("cfg4", n=3000, start=s0) for s0 in (0, 3000, 6000, 9000, 12000)]
