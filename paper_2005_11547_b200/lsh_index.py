@@ -17,7 +17,6 @@ kept on the host, like the reference's dict keys.
 
 from __future__ import annotations
 
-import ctypes
 import math
 
 import numpy as np
@@ -224,5 +223,3 @@ class LshIndex:
             r.sort(key=lambda item: (-item[1], item[0]))
         return out
 
-
-_ = ctypes
