@@ -1,4 +1,7 @@
 // dsk_lsh_kernel.cuh -- K5: (L, K) LSH table keys (included by dsk_kernels.cu).
+#ifndef DSK_LSH_CLOSE
+#define DSK_LSH_CLOSE 1  // drop hits of buckets already full when the band began
+#endif
 #ifndef DSK_LSH_FAST
 #define DSK_LSH_FAST 1  // 0: exact sort only; 1: float-key sort + exact fallback; 2: timing only
 #endif
@@ -29,11 +32,20 @@ struct LshSink {
   ModU32 md;
   uint32_t K;
   unsigned int *total;  // smem: buffered hits
-  unsigned int *cnt;    // smem: hits per bucket
+  unsigned int *cnt;    // smem: buffered hits per bucket
+  const unsigned int *prev;  // smem: cnt at the start of this band
   unsigned int *full;   // smem: buckets holding >= K hits
   int *overflow;
 
+  // Bands are rank-ordered, so a bucket that held >= K darts when this band
+  // began can never take a dart of this band into its K smallest: those hits
+  // are not buffered (they still count toward H(phi*) in the engine).
   __device__ void hit(bool valid, const HitInfo &h, int lane) {
+    uint32_t bucket = 0;
+    if (valid) {
+      bucket = mod_u32(h.bhash, md);
+      if (DSK_LSH_CLOSE && prev[bucket] >= K) valid = false;
+    }
     unsigned b = __ballot_sync(DSK_FULL, valid);
     if (b == 0) return;
     unsigned base = 0;
@@ -41,7 +53,6 @@ struct LshSink {
     base = __shfl_sync(DSK_FULL, base, 0);
     if (valid) {
       uint32_t idx = base + __popc(b & ((1u << lane) - 1));
-      uint32_t bucket = mod_u32(h.bhash, md);
       if (idx < cap) {
         buf[idx] = make_ulonglong2(h.fp, (unsigned long long)__double_as_longlong(h.rank));
         bkt[idx] = bucket;
@@ -121,6 +132,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   sink.K = (uint32_t)K;
   sink.total = &C.total;
   sink.cnt = cnt;
+  sink.prev = off;  // off[] is free until the selection's scan
   sink.full = fullc;
   sink.overflow = &C.overflow;
 
@@ -130,7 +142,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
     const long long s = C.set;
     if (s >= a.n) break;
     const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
-    for (int i = tt; i < L; i += G * 32) cnt[i] = 0;
+    for (int i = tt; i < L; i += G * 32) cnt[i] = off[i] = 0;
     if (tt == 0) {
       C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0;
       C.areas[0] = C.areas[1] = 0.0; C.chunk[0] = C.chunk[1] = 0;
@@ -177,6 +189,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         const unsigned full = *fullc;
         const bool ovf = C.overflow != 0;
         if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
+        for (int i = tt; i < L; i += G * 32) off[i] = cnt[i];  // band snapshot
         team_sync(G, team);
         if (ab || areas > kMaxAreas) { status = DSK_AREAS; break; }  // ref/darthash.py:243
         if (ovf) { status = DSK_SCRATCH; break; }
