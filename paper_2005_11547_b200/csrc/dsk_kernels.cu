@@ -59,6 +59,7 @@ struct dsk_ctx {
   void *scratch[kScratchSlots] = {};
   size_t scratch_bytes[kScratchSlots] = {};
   cudaEvent_t scratch_last[kScratchSlots] = {};
+  cudaStream_t scratch_stream[kScratchSlots] = {};  // stream of the slot's last launch
   unsigned scratch_next = 0;
 };
 
@@ -336,6 +337,12 @@ __device__ __forceinline__ void poisson_regs(PassParams &P, const SmemTables &T)
 __device__ __forceinline__ int opaque_int(int v) {
 #if DSK_OPAQUE
   asm volatile("" : "+r"(v));
+#endif
+  return v;
+}
+__device__ __forceinline__ size_t opaque_size(size_t v) {
+#if DSK_OPAQUE
+  asm volatile("" : "+l"(v));
 #endif
   return v;
 }
@@ -826,7 +833,17 @@ static bool choose_shape(const dsk_ctx *c, SmemFn smem_of, int64_t n, int &nw_ou
 // release (after its launch), so concurrent calls on different streams never
 // share a buffer and a reused slot waits for its previous launch.
 static int scratch_acquire(dsk_ctx *c, size_t need, cudaStream_t st, int &slot, void *&ptr) {
-  slot = (int)(c->scratch_next++ % dsk_ctx::kScratchSlots);
+  // prefer the slot last used on this stream (stream order already
+  // serialises it), then an unused slot, then an idle one, then round robin
+  slot = -1;
+  for (int i = 0; i < dsk_ctx::kScratchSlots && slot < 0; i++)
+    if (c->scratch[i] && c->scratch_stream[i] == st) slot = i;
+  for (int i = 0; i < dsk_ctx::kScratchSlots && slot < 0; i++)
+    if (!c->scratch[i]) slot = i;
+  for (int i = 0; i < dsk_ctx::kScratchSlots && slot < 0; i++)
+    if (cudaEventQuery(c->scratch_last[i]) == cudaSuccess) slot = i;
+  if (slot < 0) slot = (int)(c->scratch_next++ % dsk_ctx::kScratchSlots);
+  c->scratch_stream[slot] = st;
   if (!c->scratch_last[slot])
     CUDA_TRY(cudaEventCreateWithFlags(&c->scratch_last[slot], cudaEventDisableTiming));
   else

@@ -1,4 +1,7 @@
 // dsk_lsh_kernel.cuh -- K5: (L, K) LSH table keys (included by dsk_kernels.cu).
+#ifndef DSK_OPAQUE_TB
+#define DSK_OPAQUE_TB 1  // team block offsets opaque to the compiler (no rematerialisation)
+#endif
 #ifndef DSK_LSH_CLOSE
 #define DSK_LSH_CLOSE 1  // drop hits of buckets already full when the band began
 #endif
@@ -108,7 +111,11 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
             tt = opaque_team(wit * 32 + lane);
   const int L = a.L, K = a.K;
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
+#if DSK_OPAQUE_TB
+  unsigned char *tb = smem + opaque_int((int)(off_team(NW) + team * lsh_team_bytes(L)));
+#else
   unsigned char *tb = smem + off_team(NW) + team * lsh_team_bytes(L);
+#endif
   TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
   unsigned int *cnt = reinterpret_cast<unsigned int *>(tb + kTeamCtlBytes);
   unsigned int *off = cnt + L;
@@ -117,7 +124,11 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
                                                          align16((size_t)3 * L * sizeof(unsigned)));
   // global scratch of this team
   const int teams = NW / G;
+#if DSK_OPAQUE_TB
+  unsigned char *gs = a.scratch + opaque_size(((size_t)blockIdx.x * teams + team) * a.team_scratch);
+#else
   unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
+#endif
   ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
   uint32_t *bkt = reinterpret_cast<uint32_t *>(gs + (size_t)a.cap * 16);
   uint32_t *order = bkt + a.cap;
