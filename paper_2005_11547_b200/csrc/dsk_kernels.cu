@@ -29,6 +29,9 @@
 #ifndef DSK_OPAQUE
 #define DSK_OPAQUE 1
 #endif
+#ifndef DSK_OPAQUE_TB
+#define DSK_OPAQUE_TB 1  // LSH team block offsets opaque to the compiler (no rematerialisation)
+#endif
 
 using namespace dsk;
 

@@ -1,7 +1,4 @@
 // dsk_lsh_kernel.cuh -- K5: (L, K) LSH table keys (included by dsk_kernels.cu).
-#ifndef DSK_OPAQUE_TB
-#define DSK_OPAQUE_TB 1  // team block offsets opaque to the compiler (no rematerialisation)
-#endif
 #ifndef DSK_LSH_CLOSE
 #define DSK_LSH_CLOSE 1  // drop hits of buckets already full when the band began
 #endif
