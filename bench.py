@@ -12,7 +12,9 @@ scaling, no data-path collective: the sets are independent).
 Prints ONE JSON line (rank 0).  Extra keys:
   roofline      ALU bound: algorithmic hash evaluations (A + 2D + 2H per set,
                 SURVEY.md §8(d)) per second vs the K0 peak hash rate measured
-                in the same run; roofline_hbm gives the HBM view.
+                in the same run; roofline_hbm gives the HBM view and
+                roofline_issue the warp-instruction issue rate (the resource
+                the kernel is actually bound by, ~65 % busy per ncu).
   cpu_baseline  the C oracle port of the reference on the host's cores.
   e2e           the same metric through the C ABI with host buffers
                 (dsk_minhash_csr_host), H2D + D2H inside the timed region.
@@ -348,14 +350,23 @@ def main():
 
     if rank == 0:
         traffic = None
+        issue = None
         tkey = cfg.name if args.k is None else f"{cfg.name}_k{k}"
         tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
-        if os.path.exists(tpath) and args.sets is None:
-            entry = json.load(open(tpath)).get(tkey)
-            if entry:
-                traffic = {"bytes_per_launch": entry["bytes_per_launch"],
-                           "algorithmic_bytes_per_launch": hbm_bytes,
-                           "source": entry["source"]}
+        entry = json.load(open(tpath)).get(tkey) if os.path.exists(tpath) else None
+        if entry and args.sets is None:
+            traffic = {"bytes_per_launch": entry["bytes_per_launch"],
+                       "algorithmic_bytes_per_launch": hbm_bytes,
+                       "source": entry["source"]}
+        if entry and "warp_instructions_per_set" in entry and clk.get("sm_mhz"):
+            # the binding resource: warp-instruction issue (4 per SM per clock)
+            ips = entry["warp_instructions_per_set"] * n / (ms_max / 1e3)
+            peak_ips = 4.0 * torch.cuda.get_device_properties(dev).multi_processor_count * \
+                float(clk["sm_mhz"]) * 1e6
+            issue = {"bound": "issue", "achieved": ips / 1e9, "peak": peak_ips / 1e9,
+                     "unit": "G warp-inst/s", "frac": ips / peak_ips,
+                     "note": "ncu instruction count per set (profiles/ncu_traffic.json) x sets / "
+                             "kernel time, against 4 issues/clk/SM at the sampled SM clock"}
         achieved = hashes_all / sec / 1e9
         peak = peak_hps / 1e9
         line = {
@@ -384,6 +395,7 @@ def main():
                              "peak": peak_hbm, "unit": "GB/s",
                              "frac": hbm_bytes / sec / 1e9 / peak_hbm,
                              "note": "16 B/nonzero + 8 B/set + outputs; peak = MEASURED_PEAKS.json"},
+            "roofline_issue": issue,
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": args.steps,
