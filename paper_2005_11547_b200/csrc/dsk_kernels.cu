@@ -807,21 +807,27 @@ static bool team_size_ok(int G, int nw) { return nw % G == 0 && (G == 1 || nw / 
 // team, so the warps of a CTA share few sets and each set finishes sooner.
 template <class SmemFn>
 static bool choose_shape(const dsk_ctx *c, SmemFn smem_of, int64_t n, int &nw_out,
-                         int &g_out) {
+                         int &g_out, int wide_g = 0) {
+  // wide_g > 0: the widest CTA whose smallest team is <= max(that, best)
+  // wins (LSH measured faster at 24 warps in teams of 2 than 22 in teams of 1)
   int best_g = 1 << 30, best_nw = 0;       // large-batch rule
+  int wide_nw = 0, wide_gm = 0;
   int wave_g = 0, wave_nw = 0;             // one-wave rule
   const char *force = getenv("DSK_NW");  // tuning: restrict to one CTA width
   for (int nw : kWidths) {
     if (force && atoi(force) != nw) continue;
     int gmin = 0;
-    for (int G = 1; G <= nw; G++) {
+    const char *gforce = getenv("DSK_GMIN");  // tuning: smallest team size allowed
+    for (int G = gforce ? atoi(gforce) : 1; G <= nw; G++) {
       if (!team_size_ok(G, nw) || smem_of(G, nw) > c->max_smem) continue;
       if (!gmin) gmin = G;
       if ((int64_t)c->num_sms * (nw / G) >= n && G > wave_g) { wave_g = G; wave_nw = nw; }
     }
     if (gmin && gmin < best_g) { best_g = gmin; best_nw = nw; }
+    if (gmin && !wide_nw && gmin <= wide_g) { wide_nw = nw; wide_gm = gmin; }
   }
   if (!best_nw) return false;
+  if (wide_nw && wide_nw > best_nw) { best_nw = wide_nw; best_g = wide_gm; }
   if (wave_nw && !getenv("DSK_NO_WAVE")) {
     nw_out = wave_nw;
     g_out = wave_g;

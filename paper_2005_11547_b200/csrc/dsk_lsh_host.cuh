@@ -10,7 +10,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   int64_t t = (int64_t)L * K;
   if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "L*K too large");
   int NW = 0, G = 0;
-  if (!choose_shape(c, [&](int g, int nw) { return lsh_smem(L, g, nw); }, n, NW, G))
+  if (!choose_shape(c, [&](int g, int nw) { return lsh_smem(L, g, nw); }, n, NW, G, 2))
     return set_err(DSK_EUNSUPPORTED, "L too large for the shared-memory bucket counters");
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
