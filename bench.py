@@ -354,7 +354,7 @@ def main():
         tkey = cfg.name if args.k is None else f"{cfg.name}_k{k}"
         tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
         entry = json.load(open(tpath)).get(tkey) if os.path.exists(tpath) else None
-        if entry and args.sets is None:
+        if entry and args.sets is None and "bytes_per_launch" in entry:
             traffic = {"bytes_per_launch": entry["bytes_per_launch"],
                        "algorithmic_bytes_per_launch": hbm_bytes,
                        "source": entry["source"]}

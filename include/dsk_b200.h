@@ -77,6 +77,14 @@ int dsk_minhash_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
                     uint64_t *out_bits, int32_t *status, int32_t *phi, uint32_t *stats,
                     void *stream);
 
+/* dsk_minhash_csr with a hint for the CTA shape: nnz_hint = total nonzeros
+ * of the batch (0 = unknown).  Results are identical; only the team shape
+ * (warps per set) depends on it. */
+int dsk_minhash_csr_ex(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                       const double *weights, int64_t n, int32_t k, int64_t nnz_hint,
+                       uint64_t *out_values, uint64_t *out_bits, int32_t *status, int32_t *phi,
+                       uint32_t *stats, void *stream);
+
 /* The same call with HOST buffers: copies inputs in, sketches, copies the
  * results out, synchronously.  This is the drop-in a ctypes binding of the
  * reference would call with numpy arrays.  Rows are pipelined in chunks of

@@ -431,9 +431,9 @@ def minhash_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, values: b
     phi = torch.empty(n, dtype=torch.int32, device=dev)
     st = torch.empty((n, 4), dtype=torch.int32, device=dev) if stats else None
     with torch.cuda.device(dev):
-        _lib.check(_lib.load().dsk_minhash_csr(
-            hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, int(k), _ptr(out_v), _ptr(out_b),
-            _ptr(status), _ptr(phi), _ptr(st), _stream_ptr(dev)), "dsk_minhash_csr")
+        _lib.check(_lib.load().dsk_minhash_csr_ex(
+            hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, int(k), i.numel(), _ptr(out_v),
+            _ptr(out_b), _ptr(status), _ptr(phi), _ptr(st), _stream_ptr(dev)), "dsk_minhash_csr")
     res = MinhashBatch(out_v, out_b, status, phi, st)
     if check:
         raise_for_status(status)
