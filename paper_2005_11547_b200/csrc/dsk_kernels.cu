@@ -29,6 +29,9 @@
 #ifndef DSK_OPAQUE
 #define DSK_OPAQUE 1
 #endif
+#ifndef DSK_LPT
+#define DSK_LPT 1  // largest-first row order for multi-wave minhash launches
+#endif
 #ifndef DSK_OPAQUE_TB
 #define DSK_OPAQUE_TB 1  // LSH team block offsets opaque to the compiler (no rematerialisation)
 #endif
@@ -238,6 +241,8 @@ struct MinhashArgs {
   uint32_t *stats;
   unsigned long long *counter;
   uint64_t *gslots;  // non-null: slot arrays in global memory, 2*k words per team
+  const uint32_t *order;  // non-null: rows in processing order (largest first)
+  const unsigned *order_on;  // device flag: the order differs from the identity
   TableArgs tabs;
 };
 
@@ -381,7 +386,10 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   sink.tie = &C.tie;
 
   for (;;) {
-    if (tt == 0) C.set = (long long)atomicAdd(a.counter, 1ULL);
+    if (tt == 0) {
+      long long q = (long long)atomicAdd(a.counter, 1ULL);
+      C.set = (a.order && q < a.n && *a.order_on) ? (long long)a.order[q] : q;
+    }
     team_sync(G, team);
     const long long s = C.set;
     if (s >= a.n) break;
@@ -874,6 +882,51 @@ static int scratch_release(dsk_ctx *c, int slot, cudaStream_t st) {
   return DSK_OK;
 }
 
+// Largest-first processing order for multi-wave launches: rows grouped by
+// floor(log2(nnz)) classes, largest class first (an approximate LPT order:
+// the heavy tail of Zipf-sized batches no longer finishes last).
+constexpr int kSizeClasses = 32;
+
+__device__ __forceinline__ int size_class(int64_t nnz) {
+  return nnz <= 1 ? 0 : 63 - __clzll((unsigned long long)nnz);  // < 32 for nnz < 2^32
+}
+
+__global__ void order_hist_kernel(const int64_t *indptr, int64_t n, unsigned *hist) {
+  __shared__ unsigned h[kSizeClasses];
+  if (threadIdx.x < kSizeClasses) h[threadIdx.x] = 0;
+  __syncthreads();
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    atomicAdd(&h[size_class(indptr[r + 1] - indptr[r])], 1u);
+  __syncthreads();
+  if (threadIdx.x < kSizeClasses && h[threadIdx.x]) atomicAdd(&hist[threadIdx.x], h[threadIdx.x]);
+}
+
+// cursor[kSizeClasses] receives the "skewed" flag: with all rows in one
+// size class the order stays the identity (the minhash kernel ignores it)
+__global__ void order_scatter_kernel(const int64_t *indptr, int64_t n, const unsigned *hist,
+                                     unsigned *cursor, uint32_t *order) {
+  __shared__ unsigned start[kSizeClasses];
+  __shared__ bool one_class;
+  if (threadIdx.x == 0) {  // exclusive scan, largest class first
+    unsigned acc = 0, mx = 0;
+    for (int c = kSizeClasses - 1; c >= 0; c--) {
+      start[c] = acc;
+      acc += hist[c];
+      mx = hist[c] > mx ? hist[c] : mx;
+    }
+    one_class = (int64_t)mx == n;
+    if (blockIdx.x == 0) cursor[kSizeClasses] = one_class ? 0u : 1u;
+  }
+  __syncthreads();
+  if (one_class) return;
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x) {
+    int c = size_class(indptr[r + 1] - indptr[r]);
+    order[start[c] + atomicAdd(&cursor[c], 1u)] = (uint32_t)r;
+  }
+}
+
 extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                                const double *weights, int64_t n, int32_t k, uint64_t *out_values,
                                uint64_t *out_bits, int32_t *status, int32_t *phi, uint32_t *stats,
@@ -917,17 +970,34 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
   a.out_values = out_values; a.out_bits = out_bits; a.status = status; a.phi = phi;
   a.stats = stats; a.counter = counter; a.tabs = table_args(c, (double)t);
   a.gslots = nullptr;
+  a.order = nullptr;
+  a.order_on = nullptr;
   size_t smem = minhash_smem(k, G, NW, global_slots);
   int grid = c->num_sms;
   if ((int64_t)grid * (NW / G) > n) grid = (int)((n + (NW / G) - 1) / (NW / G));
+  // largest-first order when the batch spans several waves of teams
+  const bool lpt = DSK_LPT && n >= 4 * (int64_t)grid * (NW / G) && n < (1LL << 32);
   std::unique_lock<std::mutex> lock(c->scratch_mu, std::defer_lock);
   int slot = -1;
-  if (global_slots) {
+  if (global_slots || lpt) {
     lock.lock();
     void *p = nullptr;
-    int rc = scratch_acquire(c, (size_t)grid * (NW / G) * 16 * (size_t)k, st, slot, p);
+    const size_t slot_bytes = global_slots ? (size_t)grid * (NW / G) * 16 * (size_t)k : 0;
+    const size_t order_off = align16(slot_bytes);
+    const size_t need = order_off + (lpt ? align16((size_t)n * 4) + 2 * kSizeClasses * 4 + 16 : 0);
+    int rc = scratch_acquire(c, need, st, slot, p);
     if (rc) return rc;
-    a.gslots = (uint64_t *)p;
+    if (global_slots) a.gslots = (uint64_t *)p;
+    if (lpt) {
+      uint32_t *order = (uint32_t *)((char *)p + order_off);
+      unsigned *hist = (unsigned *)((char *)order + align16((size_t)n * 4));
+      CUDA_TRY(cudaMemsetAsync(hist, 0, 2 * kSizeClasses * 4 + 16, st));
+      int og = (int)((n + 255) / 256 < 4 * c->num_sms ? (n + 255) / 256 : 4 * c->num_sms);
+      order_hist_kernel<<<og, 256, 0, st>>>(indptr, n, hist);
+      order_scatter_kernel<<<og, 256, 0, st>>>(indptr, n, hist, hist + kSizeClasses, order);
+      a.order = order;
+      a.order_on = hist + 2 * kSizeClasses;
+    }
   }
   if (global_slots) {
     minhash_kernel<20, true><<<grid, 20 * 32, smem, st>>>(a);

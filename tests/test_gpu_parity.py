@@ -247,6 +247,12 @@ def test_minhash_cfg5_vs_oracle():
     _oracle_compare("cfg5", 128, 4000, start=200000)
 
 
+def test_minhash_cfg5_largest_first_order_vs_oracle():
+    # 20000 heavy-tailed rows span several waves of teams: the launch
+    # processes them largest size class first (outputs stay in row order)
+    _oracle_compare("cfg5", 128, 20000, start=500000)
+
+
 def test_minhash_odd_k_vs_oracle():
     # non-power-of-two bucket counts exercise the 64-bit modulo
     for k in (1, 3, 100, 333, 2000):
