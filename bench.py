@@ -271,10 +271,12 @@ def main():
     clocks.start()
     time.sleep(0.3)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = lib.dsk_launch_count()
     start.record()
     for _ in range(args.steps):
         res = step()
     end.record()
+    launches = int(lib.dsk_launch_count() - launches0)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -398,7 +400,7 @@ def main():
             "roofline_issue": issue,
             "e2e": e2e,
             "cpu_baseline": cpu,
-            "gpu_launches": args.steps,
+            "gpu_launches": launches,
             "clocks": clk,
             "status_nonzero": bad,
             "phi_hist": np.bincount(stats[:, 3]).tolist(),

@@ -173,6 +173,10 @@ int dsk_exact_jaccard(const int64_t *a_ptr, const uint64_t *a_ids, const double 
                       const int64_t *pa, const int64_t *pb, int64_t npairs, double *out,
                       void *stream);
 
+/* Number of kernels this library has launched in the process so far (all
+ * entry points and contexts); a caller brackets a region with two reads. */
+uint64_t dsk_launch_count(void);
+
 const char *dsk_last_error(void);
 
 #ifdef __cplusplus

@@ -72,6 +72,11 @@ struct dsk_ctx {
 constexpr int kCounterSlots = 256;
 
 static thread_local std::string g_err;
+static std::atomic<unsigned long long> g_launches{0};  // kernels launched by this library
+
+static inline void count_launch(unsigned k = 1) { g_launches.fetch_add(k); }
+
+extern "C" uint64_t dsk_launch_count(void) { return g_launches.load(); }
 
 static int set_err(int code, const char *msg) {
   g_err = msg;
@@ -993,20 +998,21 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
       unsigned *hist = (unsigned *)((char *)order + align16((size_t)n * 4));
       CUDA_TRY(cudaMemsetAsync(hist, 0, 2 * kSizeClasses * 4 + 16, st));
       int og = (int)((n + 255) / 256 < 4 * c->num_sms ? (n + 255) / 256 : 4 * c->num_sms);
-      order_hist_kernel<<<og, 256, 0, st>>>(indptr, n, hist);
-      order_scatter_kernel<<<og, 256, 0, st>>>(indptr, n, hist, hist + kSizeClasses, order);
+      order_hist_kernel<<<og, 256, 0, st>>>(indptr, n, hist); count_launch();
+      order_scatter_kernel<<<og, 256, 0, st>>>(indptr, n, hist, hist + kSizeClasses, order); count_launch();
       a.order = order;
       a.order_on = hist + 2 * kSizeClasses;
     }
   }
   if (global_slots) {
-    minhash_kernel<20, true><<<grid, 20 * 32, smem, st>>>(a);
+    minhash_kernel<20, true><<<grid, 20 * 32, smem, st>>>(a); count_launch();
   } else {
     switch (NW) {
       case 24: minhash_kernel<24><<<grid, 24 * 32, smem, st>>>(a); break;
       case 22: minhash_kernel<22><<<grid, 22 * 32, smem, st>>>(a); break;
       default: minhash_kernel<20><<<grid, 20 * 32, smem, st>>>(a); break;
     }
+    count_launch();
   }
   CUDA_TRY(cudaGetLastError());
   if (slot >= 0) return scratch_release(c, slot, st);
@@ -1038,7 +1044,7 @@ extern "C" int dsk_darts_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *
                 kWarps * kRwin * sizeof(uint4) + kWarps * sizeof(PassParams);
   int grid = (int)((n + kWarps - 1) / kWarps);
   if (grid > c->num_sms) grid = c->num_sms;
-  darts_kernel<<<grid, kWarps * 32, smem, st>>>(a);
+  darts_kernel<<<grid, kWarps * 32, smem, st>>>(a); count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
 }
@@ -1053,7 +1059,7 @@ extern "C" int dsk_hash64(dsk_ctx *c, const uint64_t *element, const uint64_t *n
   int grid = (int)((n + 255) / 256);
   if (grid > c->num_sms * 8) grid = c->num_sms * 8;
   hash64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(c->d_tab, element, nu, rho, w, r, j,
-                                                         stream_tag, n, out);
+                                                         stream_tag, n, out); count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
 }
@@ -1065,7 +1071,7 @@ extern "C" int dsk_mix64(dsk_ctx *c, const uint64_t *values, int64_t nseq, int32
   CUDA_TRY(cudaSetDevice(c->device));
   int grid = (int)((nseq + 255) / 256);
   if (grid > c->num_sms * 8) grid = c->num_sms * 8;
-  mix64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(c->d_tab, values, nseq, len, out);
+  mix64_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(c->d_tab, values, nseq, len, out); count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
 }
@@ -1077,7 +1083,7 @@ extern "C" int dsk_pack_onebit(const uint64_t *values, int64_t n, int32_t k, uin
   int64_t warps = n * ((k + 63) / 64);
   int grid = (int)((warps * 32 + 255) / 256);
   if (grid > 148 * 16) grid = 148 * 16;
-  pack_onebit_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(values, n, k, out_bits);
+  pack_onebit_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(values, n, k, out_bits); count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
 }
@@ -1087,7 +1093,7 @@ extern "C" int dsk_hash_peak(dsk_ctx *c, int32_t mode, int64_t n_per_thread, uin
   if (!c || n_per_thread < 1 || !sink) return set_err(DSK_EARG, "bad argument");
   CUDA_TRY(cudaSetDevice(c->device));
   int grid = c->num_sms * 4;
-  hash_peak_kernel<<<grid, 512, 0, (cudaStream_t)stream>>>(c->d_tab, n_per_thread, mode, sink);
+  hash_peak_kernel<<<grid, 512, 0, (cudaStream_t)stream>>>(c->d_tab, n_per_thread, mode, sink); count_launch();
   CUDA_TRY(cudaGetLastError());
   if (hashes_done) *hashes_done = (int64_t)grid * 512 * 4 * n_per_thread;
   return DSK_OK;

@@ -45,6 +45,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     case 22: lsh_kernel<22><<<grid, 22 * 32, lsh_smem(L, G, NW), st>>>(a); break;
     default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
   }
+  count_launch();
   CUDA_TRY(cudaGetLastError());
   return scratch_release(c, slot, st);
 }
