@@ -215,10 +215,18 @@ def main():
     from paper_2005_11547_b200 import workloads
 
     rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # one rank per GPU; DSK_DIST_BACKEND=gloo (+ more ranks than GPUs) is only
+    # for exercising the multi-rank code path on a one-GPU box, never timed
+    backend = os.environ.get("DSK_DIST_BACKEND", "nccl")
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    red_dev = dev if backend == "nccl" else torch.device("cpu")  # reduction tensors
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     cfg = workloads.CONFIGS[args.workload]
     k = args.k or (cfg.k[0] if cfg.k else 0)
     n = args.sets or cfg.n
@@ -264,7 +272,7 @@ def main():
     peak_hps = hash_rate(0, 256)          # full 22-lookup tabulation hash (reference's unit)
     peak_hoisted_hps = hash_rate(1, 4096)  # one lookup + finalizer (hoisted lower bound on cost)
 
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(local_dev)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -282,7 +290,7 @@ def main():
         dist.barrier()
     clk = clocks.stop()
     ms = start.elapsed_time(end) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -290,7 +298,7 @@ def main():
     # work units: areas A, candidate darts D, hits H at phi*
     A, D, H = stats[:, 0].sum(), stats[:, 1].sum(), stats[:, 2].sum()
     hashes = A + 2 * D + 2 * H + (cfg.L * cfg.K * n if cfg.kind == "lsh" else 0)
-    tot = torch.tensor([float(n), float(H), float(hashes)], dtype=torch.float64, device=dev)
+    tot = torch.tensor([float(n), float(H), float(hashes)], dtype=torch.float64, device=red_dev)
     if world > 1:
         dist.all_reduce(tot)
     sets_all, hits_all, hashes_all = (float(x) for x in tot.tolist())
@@ -335,7 +343,7 @@ def main():
         for _ in range(args.steps):
             host_call()
         dt = (time.perf_counter() - t0) / args.steps
-        tt = torch.tensor([dt], dtype=torch.float64, device=dev)
+        tt = torch.tensor([dt], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
