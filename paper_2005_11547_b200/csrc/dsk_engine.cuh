@@ -185,6 +185,11 @@ __device__ __noinline__ void rank_windows_slow(const PassParams &P, int nu, int 
   }
 }
 
+__device__ __forceinline__ uint32_t add_sat(uint32_t a, uint32_t b) {
+  uint32_t r = a + b;
+  return (r < a || r > 0x80000000u) ? 0x80000000u : r;
+}
+
 template <class Sink, bool kFull>
 struct Engine {
   const SmemTables &T;
@@ -201,7 +206,9 @@ struct Engine {
   bool use_table = false;
   bool direct = false;      // rho = 0 areas come from per-lane walkers, not the region ring
   bool abort = false;       // warp-uniform: area cap exceeded by one lane's share
-  double lane_full = 0.0;   // per lane: areas of the full (non-band) step (area cap)
+  // per lane: areas of the full (non-band) step (area cap); saturates at
+  // 2^31, far above the 2^27 cap, so sums stay exact wherever they matter
+  uint32_t lane_full = 0;
   uint32_t n_darts = 0;     // per lane: candidate darts first seen in this band
   uint32_t n_hits = 0;      // per lane
   // element chunk state: lane i holds element i's region-count scan
@@ -511,7 +518,7 @@ struct Engine {
       if (dtop >= 0) {
         uint4 rw = rwin[dtop * (P.RD + 1)];
         cnt0 = rw.z;
-        lane_full += (double)rw.w;
+        lane_full = add_sat(lane_full, rw.w);
       }
       nruns = (cnt0 + kRun - 1) / kRun;
       dmeta = (uint32_t)(dtop & 0xff) | ((uint32_t)nu_v << 8);
@@ -679,7 +686,7 @@ struct Engine {
         bool okq = w_hi >= 0 && r_lo <= r_hi;
         if (w_hi >= 0) {
           double full = (double)(w_hi + 1) * (double)(r_hi + 1);
-          lane_full += full;
+          lane_full = add_sat(lane_full, full >= 2147483648.0 ? 0x80000000u : (uint32_t)full);
           // a region over the cap makes the step illegal (ref/darthash.py:242-244)
           if (full > kMaxAreas) okq = false;
         }
@@ -755,7 +762,7 @@ struct Engine {
   }
 
   __device__ double warp_full() const {
-    double s = lane_full;
+    double s = (double)lane_full;
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(DSK_FULL, s, o);
     return s;

@@ -15,8 +15,8 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "lpt1": {},
-    "lpt0": {"DSK_LPT": 0},
+    "lf32": {},
+    "base": {},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
