@@ -339,19 +339,22 @@ def main():
         host_call()
         if world > 1:
             dist.barrier()
+        b0 = lib.dsk_h2d_bytes()
         t0 = time.perf_counter()
         for _ in range(args.steps):
             host_call()
         dt = (time.perf_counter() - t0) / args.steps
+        h2d_copied = (lib.dsk_h2d_bytes() - b0) // args.steps
         tt = torch.tensor([dt], dtype=torch.float64, device=red_dev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         dt = float(tt.item())
-        h2d = indptr.nbytes + ids.nbytes + w.nbytes
+        h2d = int(h2d_copied)  # as counted by the library (dsk_h2d_bytes)
         d2h = o_v.numel() * 8 + o_s.numel() * 4 + (o_b.numel() * 8 if o_b is not None else 0)
         e2e = {"value": sets_all / dt, "unit": "sketches/sec", "ms_per_step": dt * 1000.0,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "api": f"{api} (C ABI, pinned host buffers)"}
+               "api": f"{api} (C ABI, pinned host buffers)",
+               "input_bytes_per_step": int(indptr.nbytes + ids.nbytes + w.nbytes)}
         assert (o_s.numpy() == 0).all()
 
     cpu = None

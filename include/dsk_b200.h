@@ -177,6 +177,9 @@ int dsk_exact_jaccard(const int64_t *a_ptr, const uint64_t *a_ids, const double 
  * entry points and contexts); a caller brackets a region with two reads. */
 uint64_t dsk_launch_count(void);
 
+/* Bytes the host-buffer entry points have copied host -> device so far. */
+uint64_t dsk_h2d_bytes(void);
+
 const char *dsk_last_error(void);
 
 #ifdef __cplusplus

@@ -1165,11 +1165,19 @@ static size_t host_chunk_cap() {
   return mb << 20;
 }
 
+static std::atomic<unsigned long long> g_h2d_bytes{0};  // bytes copied in by host-buffer calls
+
+extern "C" uint64_t dsk_h2d_bytes(void) { return g_h2d_bytes.load(); }
+
 // Drive the pipeline.  launch(r0, m, stream) sketches rows [r0, r0 + m)
 // reading the staged input; out(r0, m, stream) copies their results back.
 // dp/di/dw are the staged indptr/ids/weights.  With two compute streams the
 // CTAs of chunk c + 1 take over SMs as chunk c's persistent CTAs retire, so
 // launch tails overlap (LSH launches take separate scratch slots).
+//
+// (Narrowing ids to u32 on the host before the copy was tried: 16 host
+// threads narrowing while the DMA engine reads the same host memory made the
+// cfg2 e2e step slower, 43.6 ms against 31.6 ms.)
 template <class Launch, class Out>
 static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                          const double *weights, int64_t n, int64_t *dp, uint64_t *di, double *dw,
@@ -1179,24 +1187,26 @@ static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
   plan_chunks(indptr, n, host_chunk_cap(), bounds, kMaxChunks + 1, &nch);
   cudaStream_t cp = c->hs[0], os = c->hs[2];
   CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, cp));
-  for (int ch = 0; ch < nch; ch++) {
-    const int64_t e0 = indptr[bounds[ch]], e1 = indptr[bounds[ch + 1]];
-    CUDA_TRY(cudaMemcpyAsync(di + e0, ids + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, cp));
-    CUDA_TRY(cudaMemcpyAsync(dw + e0, weights + e0, (e1 - e0) * 8, cudaMemcpyHostToDevice, cp));
-    CUDA_TRY(cudaEventRecord(c->ev_in[ch], cp));
-  }
+  unsigned long long h2d = (unsigned long long)(n + 1) * 8;
   int rc = DSK_OK;
   for (int ch = 0; ch < nch && rc == DSK_OK; ch++) {
-    const int64_t r0 = bounds[ch], m = bounds[ch + 1] - r0;
+    const int64_t e0 = indptr[bounds[ch]], e1 = indptr[bounds[ch + 1]], m = e1 - e0;
+    CUDA_TRY(cudaMemcpyAsync(di + e0, ids + e0, m * 8, cudaMemcpyHostToDevice, cp));
+    h2d += (unsigned long long)m * 8;
+    CUDA_TRY(cudaMemcpyAsync(dw + e0, weights + e0, m * 8, cudaMemcpyHostToDevice, cp));
+    h2d += (unsigned long long)m * 8;
+    CUDA_TRY(cudaEventRecord(c->ev_in[ch], cp));
+    const int64_t r0 = bounds[ch], rows = bounds[ch + 1] - r0;
     cudaStream_t ks = c->hs[(compute_streams > 1 && (ch & 1)) ? 3 : 1];
     CUDA_TRY(cudaStreamWaitEvent(ks, c->ev_in[ch], 0));
-    rc = launch(r0, m, ks);
+    rc = launch(r0, rows, ks);
     if (rc) break;
     CUDA_TRY(cudaEventRecord(c->ev_k[ch], ks));
     CUDA_TRY(cudaStreamWaitEvent(os, c->ev_k[ch], 0));
-    rc = out(r0, m, os);
+    rc = out(r0, rows, os);
   }
   for (int i = 0; i < 4; i++) CUDA_TRY(cudaStreamSynchronize(c->hs[i]));
+  g_h2d_bytes.fetch_add(h2d);
   return rc;
 }
 

@@ -525,6 +525,15 @@ def test_host_pipeline_many_chunks(monkeypatch, chunk_mb):
                                          None, P(status), None, None)
     assert rc == 0 and (status == 0).all()
     assert np.array_equal(vals, as_u64(dev.values))
+    # ids wider than 32 bits in the second half of the rows
+    wide = ids.copy()
+    wide[indptr[3000]:] += np.uint64(1 << 40)
+    dev_w = minhash_batch(indptr, wide, w, 64, f)
+    vals[:] = 0
+    rc = _lib.load().dsk_minhash_csr_host(f.context(), P(indptr), P(wide), P(w), 6000, 64,
+                                         P(vals), None, P(status), None, None)
+    assert rc == 0 and (status == 0).all()
+    assert np.array_equal(vals, as_u64(dev_w.values))
     indptr, ids, w = workloads.generate("cfg4", n=1500)
     dev = lsh_batch(indptr, ids, w, LshParams(30, 4), f, fps=True)
     keys = np.zeros((1500, 30), dtype=np.uint64)
