@@ -22,6 +22,7 @@ from __future__ import annotations
 import ctypes
 import dataclasses
 import math
+import threading
 from dataclasses import dataclass
 
 import numpy as np
@@ -109,7 +110,7 @@ class HashFamily:
     threads (contexts are read-only after creation).
     """
 
-    __slots__ = ("seed", "_tables", "poisson_cdf", "_ctx", "_cdf_dev")
+    __slots__ = ("seed", "_tables", "poisson_cdf", "_ctx", "_cdf_dev", "_ctx_lock")
 
     def __init__(self, seed: int):
         seed = int(seed)
@@ -118,20 +119,27 @@ class HashFamily:
         self.poisson_cdf = constants.poisson1_cdf()
         self._ctx = {}
         self._cdf_dev = {}
+        self._ctx_lock = threading.Lock()
 
     def context(self, device=None) -> ctypes.c_void_p:
+        """The libdsk_b200 context of this family on `device` (created once,
+        thread-safely; the C calls themselves are reentrant)."""
         dev = _device(device)
         ctx = self._ctx.get(dev.index)
         if ctx is None:
-            lib = _lib.load()
-            out = ctypes.c_void_p()
-            thr = constants.log2_thresholds()
-            with torch.cuda.device(dev):
-                _lib.check(lib.dsk_ctx_create(dev.index, self._tables.ctypes.data,
-                                              self.poisson_cdf.ctypes.data, thr.ctypes.data,
-                                              ctypes.byref(out)), "dsk_ctx_create")
-            ctx = out
-            self._ctx[dev.index] = ctx
+            with self._ctx_lock:
+                ctx = self._ctx.get(dev.index)
+                if ctx is None:
+                    lib = _lib.load()
+                    out = ctypes.c_void_p()
+                    thr = constants.log2_thresholds()
+                    with torch.cuda.device(dev):
+                        _lib.check(lib.dsk_ctx_create(dev.index, self._tables.ctypes.data,
+                                                      self.poisson_cdf.ctypes.data,
+                                                      thr.ctypes.data, ctypes.byref(out)),
+                                   "dsk_ctx_create")
+                    ctx = out
+                    self._ctx[dev.index] = ctx
         return ctx
 
     def __del__(self):
