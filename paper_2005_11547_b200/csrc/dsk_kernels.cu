@@ -768,6 +768,8 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<22>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,

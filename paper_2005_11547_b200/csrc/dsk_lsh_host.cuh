@@ -10,8 +10,15 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   int64_t t = (int64_t)L * K;
   if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "L*K too large");
   int NW = 0, G = 0;
-  if (!choose_shape(c, [&](int g, int nw) { return lsh_smem(L, g, nw); }, n, NW, G, 2))
-    return set_err(DSK_EUNSUPPORTED, "L too large for the shared-memory bucket counters");
+  // bucket counters in shared memory; L too large for that -> global scratch
+  bool gc = false;
+  if (!choose_shape(c, [&](int g, int nw) { return lsh_smem(L, g, nw); }, n, NW, G, 2)) {
+    gc = true;
+    if (!choose_shape(c, [&](int g, int nw) {
+          return nw == 20 ? off_team(nw) + (size_t)(nw / g) * kTeamCtlBytes : (size_t)1 << 40;
+        }, n, NW, G))
+      return set_err(DSK_EUNSUPPORTED, "no CTA shape fits shared memory");
+  }
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
   const int teams = NW / G;
@@ -19,7 +26,8 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   if ((int64_t)grid * teams > n) grid = (int)((n + teams - 1) / teams);
   // hit buffer per team: ~8 phi steps of L*K darts, at least 16K entries
   uint32_t cap = (uint32_t)(8 * t > 16384 ? 8 * t : 16384);
-  size_t team_bytes = align16((size_t)cap * 24) + align16((size_t)L * K * 8);
+  size_t team_bytes = align16((size_t)cap * 24) + align16((size_t)L * K * 8) +
+                      (gc ? align16((size_t)3 * L * sizeof(unsigned)) + 16 : 0);
   size_t need = (size_t)grid * teams * team_bytes;
   // hit buffers from the context's stream-ordered scratch pool
   std::lock_guard<std::mutex> lock(c->scratch_mu);
@@ -40,10 +48,14 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
   a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap;
   a.tabs = table_args(c, (double)t);
-  switch (NW) {
-    case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
-    case 22: lsh_kernel<22><<<grid, 22 * 32, lsh_smem(L, G, NW), st>>>(a); break;
-    default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+  if (gc) {
+    lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);
+  } else {
+    switch (NW) {
+      case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+      case 22: lsh_kernel<22><<<grid, 22 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+      default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+    }
   }
   count_launch();
   CUDA_TRY(cudaGetLastError());

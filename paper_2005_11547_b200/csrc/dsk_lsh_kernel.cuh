@@ -98,7 +98,9 @@ __host__ __device__ inline size_t lsh_smem(int L, int G, int nw) {
   return off_team(nw) + (size_t)teams * lsh_team_bytes(L);
 }
 
-template <int NW>
+// kGC: the per-bucket counters live in the team's global scratch instead of
+// shared memory (L too large for shared memory; instantiated for NW = 20)
+template <int NW, bool kGC = false>
 __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
@@ -108,17 +110,13 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
             tt = opaque_team(wit * 32 + lane);
   const int L = a.L, K = a.K;
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
+  const size_t tbytes = kGC ? kTeamCtlBytes : lsh_team_bytes(L);
 #if DSK_OPAQUE_TB
-  unsigned char *tb = smem + opaque_int((int)(off_team(NW) + team * lsh_team_bytes(L)));
+  unsigned char *tb = smem + opaque_int((int)(off_team(NW) + team * tbytes));
 #else
-  unsigned char *tb = smem + off_team(NW) + team * lsh_team_bytes(L);
+  unsigned char *tb = smem + off_team(NW) + team * tbytes;
 #endif
   TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
-  unsigned int *cnt = reinterpret_cast<unsigned int *>(tb + kTeamCtlBytes);
-  unsigned int *off = cnt + L;
-  unsigned int *cur = off + L;
-  unsigned int *fullc = reinterpret_cast<unsigned int *>(tb + kTeamCtlBytes +
-                                                         align16((size_t)3 * L * sizeof(unsigned)));
   // global scratch of this team
   const int teams = NW / G;
 #if DSK_OPAQUE_TB
@@ -126,6 +124,13 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
 #else
   unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
 #endif
+  unsigned char *cb = kGC ? gs + align16((size_t)a.cap * 24) + align16((size_t)L * K * 8)
+                          : tb + kTeamCtlBytes;
+  unsigned int *cnt = reinterpret_cast<unsigned int *>(cb);
+  unsigned int *off = cnt + L;
+  unsigned int *cur = off + L;
+  unsigned int *fullc =
+      reinterpret_cast<unsigned int *>(cb + align16((size_t)3 * L * sizeof(unsigned)));
   ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
   uint32_t *bkt = reinterpret_cast<uint32_t *>(gs + (size_t)a.cap * 16);
   uint32_t *order = bkt + a.cap;

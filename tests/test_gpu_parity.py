@@ -406,6 +406,18 @@ def test_minhash_host_multi_device_gather():
         assert np.array_equal(bits, as_u64(dev.bits))
 
 
+@pytest.mark.parametrize("L,K", [(6000, 1), (5000, 2)])
+def test_lsh_large_L_global_counters_vs_oracle(L, K):
+    """L beyond the shared-memory bucket counters: counters in global scratch."""
+    indptr, ids, w = workloads.generate("cfg1", n=5)
+    res = lsh_batch(indptr, ids, w, LshParams(L, K), fam(0), fps=True)
+    keys, fps, status, phi, _ = Oracle(0).lsh_csr(indptr, ids, w, L, K, want_fps=True)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(as_u64(res.fps), fps)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+
+
 def test_lsh_concurrent_streams():
     """LSH launches on different streams take separate hit-buffer slots."""
     parts = [workloads.generate("cfg4", n=3000, start=s0) for s0 in (0, 3000, 6000, 9000, 12000)]
