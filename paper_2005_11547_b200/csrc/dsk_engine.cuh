@@ -58,6 +58,16 @@ namespace dsk {
 #ifndef DSK_REFILL
 #define DSK_REFILL 8
 #endif
+// scheduler thresholds (<= 32: a stage runs once this many items are queued)
+#ifndef DSK_TH_HIT
+#define DSK_TH_HIT 32
+#endif
+#ifndef DSK_TH_AREA
+#define DSK_TH_AREA 32
+#endif
+#ifndef DSK_TH_REG
+#define DSK_TH_REG 32
+#endif
 #ifndef DSK_FUSE
 #define DSK_FUSE 2  // dart 0 finished at area creation: 0 never, 1 direct walkers, 2 both paths
 #endif
@@ -727,11 +737,11 @@ struct Engine {
     for (;;) {
       const bool up_area_empty = el_done && rg_cnt == 0;
       const bool up_hit_empty = up_area_empty && ar_cnt == 0;
-      if (ht_cnt >= kStep || (up_hit_empty && ht_cnt > 0)) {
+      if (ht_cnt >= DSK_TH_HIT || (up_hit_empty && ht_cnt > 0)) {
         hits_step();
-      } else if (ar_cnt >= 32 || (up_area_empty && ar_cnt > 0)) {
+      } else if (ar_cnt >= DSK_TH_AREA || (up_area_empty && ar_cnt > 0)) {
         areas_step();
-      } else if (rg_cnt >= 32 || (el_done && rg_cnt > 0)) {
+      } else if (rg_cnt >= DSK_TH_REG || (el_done && rg_cnt > 0)) {
         regions_step();
       } else if (!el_done) {
         if (direct && walkers_busy()) {
