@@ -24,9 +24,18 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   const int teams = NW / G;
   int grid = c->num_sms;
   if ((int64_t)grid * teams > n) grid = (int)((n + teams - 1) / teams);
-  // hit buffer per team: ~8 phi steps of L*K darts, at least 16K entries
-  uint32_t cap = (uint32_t)(8 * t > 16384 ? 8 * t : 16384);
-  size_t team_bytes = align16((size_t)cap * 24) + align16((size_t)L * K * 8) +
+  // hit slots per bucket: >= 64 (the register sorts) and >= about two bands
+  // of a bucket's hits past K (buffering stops once a band begins full)
+  int64_t S64 = 2 * ((int64_t)K + t / L) + 32;
+  S64 = S64 < 64 ? 64 : (S64 + 31) / 32 * 32;
+  if (S64 > (1 << 20)) S64 = 1 << 20;
+  if (const char *e = getenv("DSK_LSH_SLOTS"))  // tests: force the overflow list
+    S64 = atoi(e) > 64 ? atoi(e) : 64;
+  const uint32_t S = (uint32_t)S64;
+  // overflow list per team for buckets past their S slots (rare)
+  uint32_t cap = (uint32_t)(2 * t > 16384 ? (2 * t < (1 << 26) ? 2 * t : (1 << 26)) : 16384);
+  size_t team_bytes = align16((size_t)L * S * 16) + align16((size_t)cap * 16) +
+                      align16((size_t)cap * 4) + align16((size_t)L * K * 8) +
                       (gc ? align16((size_t)3 * L * sizeof(unsigned)) + 16 : 0);
   size_t need = (size_t)grid * teams * team_bytes;
   // hit buffers from the context's stream-ordered scratch pool
@@ -46,7 +55,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.exact_sort = ex && atoi(ex) != 0; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
   a.md = make_mod((uint32_t)L); a.G = G; a.out_keys = out_keys; a.out_fps = out_fps;
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
-  a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap;
+  a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap; a.S = S;
   a.tabs = table_args(c, (double)t);
   if (gc) {
     lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);

@@ -15,52 +15,56 @@
 //
 // Per team (G warps on one set):
 //   enumeration  the shared engine, phi bands 1, 2, ... as for minhash; the
-//                sink appends every hit {rank, fp} to a global per-team
-//                scratch (L2-resident) and counts hits per bucket in smem;
+//                sink writes every hit {fp, rank} into its bucket's slots of
+//                the team's global scratch (overflow list past S slots) and
+//                counts hits per bucket;
 //   check        after each band: all L buckets >= K (counter of buckets
 //                that reached K);
-//   selection    counting sort of the buffered hits by bucket, then for each
-//                bucket the position of every entry among its bucket by
-//                (rank bits, fp) -- positions < K are the key, in order;
+//   selection    per bucket, a register bitonic sort (<= 64 entries) or a
+//                counting rank by (rank bits, fp) -- positions < K are the
+//                key, in order;
 //   epilogue     one lane per table folds the K fingerprints with mix64.
 
 struct LshSink {
   static constexpr bool kFuse = false;
-  ulonglong2 *buf;      // global: {fp, rank bits} per buffered hit
-  uint32_t *bkt;        // global: bucket per buffered hit
-  uint32_t cap;
+  ulonglong2 *buf;      // global: {fp, rank bits}, bucket b's first S hits at b*S
+  ulonglong2 *ovf;      // global: hits beyond a bucket's S slots
+  uint32_t *ovf_b;      // global: their buckets
+  uint32_t S;           // slots per bucket
+  uint32_t cap;         // overflow capacity
   ModU32 md;
   uint32_t K;
-  unsigned int *total;  // smem: buffered hits
-  unsigned int *cnt;    // smem: buffered hits per bucket
-  const unsigned int *prev;  // smem: cnt at the start of this band
-  unsigned int *full;   // smem: buckets holding >= K hits
+  unsigned int *total;  // smem: overflow entries
+  unsigned int *cnt;    // buffered hits per bucket
+  const unsigned int *prev;  // cnt at the start of this band
+  unsigned int *full;   // buckets holding >= K hits
   int *overflow;
 
   // Bands are rank-ordered, so a bucket that held >= K darts when this band
   // began can never take a dart of this band into its K smallest: those hits
   // are not buffered (they still count toward H(phi*) in the engine).
   __device__ void hit(bool valid, const HitInfo &h, int lane) {
-    uint32_t bucket = 0;
     if (valid) {
-      bucket = mod_u32(h.bhash, md);
-      if (DSK_LSH_CLOSE && prev[bucket] >= K) valid = false;
-    }
-    unsigned b = __ballot_sync(DSK_FULL, valid);
-    if (b == 0) return;
-    unsigned base = 0;
-    if (lane == 0) base = atomicAdd(total, (unsigned)__popc(b));
-    base = __shfl_sync(DSK_FULL, base, 0);
-    if (valid) {
-      uint32_t idx = base + __popc(b & ((1u << lane) - 1));
-      if (idx < cap) {
-        buf[idx] = make_ulonglong2(h.fp, (unsigned long long)__double_as_longlong(h.rank));
-        bkt[idx] = bucket;
-      } else {
-        atomicOr(overflow, 1);
+      const uint32_t bucket = mod_u32(h.bhash, md);
+      if (!(DSK_LSH_CLOSE && prev[bucket] >= K)) {
+        const unsigned slot = atomicAdd(&cnt[bucket], 1u);
+        if (slot == K - 1) atomicAdd(full, 1u);
+        const ulonglong2 e =
+            make_ulonglong2(h.fp, (unsigned long long)__double_as_longlong(h.rank));
+        if (slot < S) {
+          buf[(size_t)bucket * S + slot] = e;
+        } else {  // rare: the bucket's slots are full
+          const unsigned o = atomicAdd(total, 1u);
+          if (o < cap) {
+            ovf[o] = e;
+            ovf_b[o] = bucket;
+          } else {
+            atomicOr(overflow, 1);
+          }
+        }
       }
-      if (atomicAdd(&cnt[bucket], 1u) == K - 1) atomicAdd(full, 1u);
     }
+    (void)lane;
   }
   __device__ void row(const DartRow &) {}
 };
@@ -84,7 +88,8 @@ struct LshArgs {
   unsigned long long *counter;
   unsigned char *scratch;  // per-team global scratch
   size_t team_scratch;     // bytes per team
-  uint32_t cap;            // buffered-hit capacity per team
+  uint32_t cap;            // overflow capacity per team
+  uint32_t S;              // slots per bucket
   TableArgs tabs;
 };
 
@@ -124,28 +129,34 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
 #else
   unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
 #endif
-  unsigned char *cb = kGC ? gs + align16((size_t)a.cap * 24) + align16((size_t)L * K * 8)
-                          : tb + kTeamCtlBytes;
+  // team scratch: slots L*S*16 | overflow cap*16 | overflow buckets cap*4 |
+  // selection L*K*8 | (kGC) counters
+  const size_t o_ovf = align16((size_t)L * a.S * 16), o_ovb = o_ovf + align16((size_t)a.cap * 16);
+  const size_t o_sel = o_ovb + align16((size_t)a.cap * 4), o_cnt = o_sel + align16((size_t)L * K * 8);
+  unsigned char *cb = kGC ? gs + o_cnt : tb + kTeamCtlBytes;
   unsigned int *cnt = reinterpret_cast<unsigned int *>(cb);
   unsigned int *off = cnt + L;
   unsigned int *cur = off + L;
   unsigned int *fullc =
       reinterpret_cast<unsigned int *>(cb + align16((size_t)3 * L * sizeof(unsigned)));
   ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
-  uint32_t *bkt = reinterpret_cast<uint32_t *>(gs + (size_t)a.cap * 16);
-  uint32_t *order = bkt + a.cap;
-  uint64_t *sel = reinterpret_cast<uint64_t *>(gs + align16((size_t)a.cap * 24));
+  ulonglong2 *ovf = reinterpret_cast<ulonglong2 *>(gs + o_ovf);
+  uint32_t *ovf_b = reinterpret_cast<uint32_t *>(gs + o_ovb);
+  uint64_t *sel = reinterpret_cast<uint64_t *>(gs + o_sel);
+  const uint32_t S = a.S;
   __syncthreads();
 
   LshSink sink;
   sink.buf = buf;
-  sink.bkt = bkt;
+  sink.ovf = ovf;
+  sink.ovf_b = ovf_b;
+  sink.S = S;
   sink.cap = a.cap;
   sink.md = a.md;
   sink.K = (uint32_t)K;
   sink.total = &C.total;
   sink.cnt = cnt;
-  sink.prev = off;  // off[] is free until the selection's scan
+  sink.prev = off;  // band-start snapshot of cnt
   sink.full = fullc;
   sink.overflow = &C.overflow;
 
@@ -198,7 +209,6 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         team_sync(G, team);
         const double areas = C.areas[par];
         const bool ab = C.abort != 0;
-        const unsigned total = C.total;
         const unsigned full = *fullc;
         const bool ovf = C.overflow != 0;
         if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
@@ -208,7 +218,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         if (ovf) { status = DSK_SCRATCH; break; }
         final_areas = areas;
         // ref/annindex.py:72-76: >= L*K darts and every bucket >= K
-        if (total >= (unsigned)(L * K) && full == (unsigned)L) {
+        if (full == (unsigned)L) {  // implies >= L*K darts
           status = DSK_OK;
           phi_star = phi;
           break;
@@ -221,24 +231,9 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
     if (lane == 0) { atomicAdd(&C.darts, wd); atomicAdd(&C.hits, wh); }
     team_sync(G, team);
     if (status == 0) {
-      // ---- selection: counting sort by bucket (ref/annindex.py:77-81)
-      const unsigned total = C.total;
-      if (wit == 0) {  // exclusive scan of the bucket counts
-        unsigned carry = 0;
-        for (int b0 = 0; b0 < L; b0 += 32) {
-          unsigned v = b0 + lane < L ? cnt[b0 + lane] : 0;
-          unsigned incl = warp_incl_scan(v, lane);
-          if (b0 + lane < L) { off[b0 + lane] = carry + incl - v; cur[b0 + lane] = 0; }
-          carry += __shfl_sync(DSK_FULL, incl, 31);
-        }
-      }
-      team_sync(G, team);
-      for (unsigned i = tt; i < total; i += G * 32) {
-        uint32_t b = bkt[i];
-        order[off[b] + atomicAdd(&cur[b], 1u)] = i;
-      }
-      __threadfence_block();
-      team_sync(G, team);
+      // ---- selection (ref/annindex.py:77-81): bucket b's hits sit in its S
+      // slots (plus, past S, in the overflow list)
+      const unsigned ovf_n = C.total < a.cap ? C.total : a.cap;
       // K smallest of each bucket by (rank bits, fp).  Buckets of <= 64
       // entries (nearly all: ~40 per bucket at cfg4's stopping step) are
       // sorted in registers with a 64-wide bitonic network, first on a packed
@@ -249,7 +244,8 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       // index tuple).
       bool tie = false;
       for (int b = wit; b < L; b += G) {
-        const unsigned o = off[b], nb = cnt[b];
+        const unsigned nb = cnt[b];
+        const size_t o = (size_t)b * S;  // bucket b's slots (nb <= 64 <= S on the register paths)
         bool exact = nb > 64 || DSK_LSH_FAST == 0 || a.exact_sort;
         if (!exact) {
           // fast path: bitonic sort of one 64-bit key per entry, the rank
@@ -262,7 +258,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           for (int h = 0; h < 2; h++) {
             unsigned i = lane + 32 * h;
             if (i < nb) {
-              uint32_t ei = order[o + i];
+              uint32_t ei = (uint32_t)(o + i);
               double rk = __longlong_as_double((long long)buf[ei].y);
               key[h] = ((unsigned long long)__float_as_uint(__double2float_rn(rk)) << 32) | ei;
             } else {
@@ -309,7 +305,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           for (int h = 0; h < 2; h++) {
             unsigned i = lane + 32 * h;
             if (i < nb) {
-              ulonglong2 e = buf[order[o + i]];
+              ulonglong2 e = buf[o + i];
               kr[h] = e.y;
               kf[h] = e.x;
             } else {
@@ -354,13 +350,24 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
             if (p < (unsigned)K) sel[(size_t)b * K + p] = kf[h];
           }
         } else if (exact) {
+          // > 64 entries: rank every entry by counting; entry m of the bucket
+          // is slot m (m < S) or the (m - S)-th overflow entry of bucket b
+          const unsigned ns = nb < S ? nb : S;
+          auto entry = [&](unsigned m, uint32_t &id) -> ulonglong2 {
+            if (m < ns) { id = (uint32_t)m; return buf[o + m]; }
+            unsigned seen = ns;
+            for (unsigned q = 0; q < ovf_n; q++)
+              if (ovf_b[q] == (uint32_t)b && seen++ == m) { id = S + q; return ovf[q]; }
+            id = 0xffffffffu;
+            return make_ulonglong2(~0ULL, ~0ULL);
+          };
           for (unsigned i = lane; i < nb; i += 32) {
-            uint32_t ei = order[o + i];
-            ulonglong2 e = buf[ei];
+            uint32_t ei;
+            ulonglong2 e = entry(i, ei);
             unsigned pos = 0;
             for (unsigned m = 0; m < nb; m++) {
-              uint32_t mi = order[o + m];
-              ulonglong2 f = buf[mi];
+              uint32_t mi;
+              ulonglong2 f = entry(m, mi);
               bool less = f.y < e.y || (f.y == e.y && (f.x < e.x || (f.x == e.x && mi < ei)));
               pos += less;
               if (f.y == e.y && mi != ei && f.x != e.x) tie = true;

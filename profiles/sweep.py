@@ -15,11 +15,8 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "th32": {},
-    "h24": {"DSK_TH_HIT": 24},
-    "a24": {"DSK_TH_AREA": 24},
-    "r24": {"DSK_TH_REG": 24},
-    "h28a28": {"DSK_TH_HIT": 28, "DSK_TH_AREA": 28},
+    "new": {},
+    "old": {},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]

@@ -418,6 +418,20 @@ def test_lsh_large_L_global_counters_vs_oracle(L, K):
     assert np.array_equal(res.phi.cpu().numpy(), phi)
 
 
+@pytest.mark.parametrize("L,K", [(1, 50), (3, 40), (2, 90)])
+def test_lsh_bucket_overflow_list_vs_oracle(monkeypatch, L, K):
+    """Buckets past their hit slots (forced to 64) spill into the overflow
+    list and are ranked by counting over slots + list."""
+    monkeypatch.setenv("DSK_LSH_SLOTS", "64")
+    indptr, ids, w = workloads.generate("cfg4", n=60, start=31)
+    res = lsh_batch(indptr, ids, w, LshParams(L, K), fam(3), fps=True)
+    keys, fps, status, phi, _ = Oracle(3).lsh_csr(indptr, ids, w, L, K, want_fps=True)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(as_u64(res.fps), fps)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+
+
 def test_lsh_concurrent_streams():
     """LSH launches on different streams take separate hit-buffer slots."""
     parts = [workloads.generate("cfg4", n=3000, start=s0) for s0 in (0, 3000, 6000, 9000, 12000)]
