@@ -1132,8 +1132,15 @@ static int ensure_stage(dsk_ctx *c, size_t bytes) {
 
 // Row chunk boundaries: chunk i carries ~min(cap, 16 MB << i, max(8 MB,
 // remaining / 2)) input bytes (16 B per nonzero + 8 B per row).
+// first chunk and smallest tail chunk in MB (env DSK_RAMP_MB="first,tail")
+static size_t kRampMB[2] = {16, 8};
+
 static void plan_chunks(const int64_t *indptr, int64_t n, size_t cap, int64_t *bounds,
                         int max_chunks, int *nchunks) {
+  if (const char *e = getenv("DSK_RAMP_MB")) {
+    int f = 0, t = 0;
+    if (sscanf(e, "%d,%d", &f, &t) == 2 && f > 0 && t > 0) { kRampMB[0] = f; kRampMB[1] = t; }
+  }
   const size_t total = (size_t)indptr[n] * 16 + (size_t)n * 8;
   if (cap < total / (max_chunks - 12)) cap = total / (max_chunks - 12) + 1;
   int m = 0;
@@ -1143,17 +1150,19 @@ static void plan_chunks(const int64_t *indptr, int64_t n, size_t cap, int64_t *b
   while (r < n && m < max_chunks) {
     const int64_t lo = r;
     size_t target = cap;
-    const size_t ramp = (size_t)16 << (20 + (m - 1 < 6 ? m - 1 : 6));
+    const size_t ramp = kRampMB[0] << (20 + (m - 1 < 6 ? m - 1 : 6));
     if (ramp < target) target = ramp;
     size_t half = (total - done) / 2;
-    if (half < ((size_t)8 << 20)) half = (size_t)8 << 20;
+    if (half < (kRampMB[1] << 20)) half = kRampMB[1] << 20;
     if (half < target) target = half;
-    int64_t step = 1;
-    while (r < n && (size_t)((indptr[r] - indptr[lo]) * 16 + (r - lo) * 8) < target) {
-      r = r + step < n ? r + step : n;
-      step = step < (1 << 16) ? step * 2 : step;
+    // largest r with bytes(lo, r) <= target (at least one row)
+    int64_t a = lo + 1, b = n;
+    while (a < b) {
+      const int64_t mid = a + (b - a + 1) / 2;
+      if ((size_t)((indptr[mid] - indptr[lo]) * 16 + (mid - lo) * 8) <= target) a = mid;
+      else b = mid - 1;
     }
-    if (r == lo) r = lo + 1;
+    r = a;
     done += (size_t)((indptr[r] - indptr[lo]) * 16 + (r - lo) * 8);
     bounds[m++] = r;
   }
