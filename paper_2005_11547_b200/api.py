@@ -472,9 +472,64 @@ def lsh_batch(indptr, ids, weights, params: LshParams, hashes: HashFamily, *,
     if check:
         raise_for_status(status)
         if bool(((status & DSK_STATUS_TIE) != 0).any()):
-            raise RuntimeError("bit-identical dart ranks in an LSH table: tie resolution for "
-                               "lsh keys is not implemented")
+            _resolve_lsh_ties(res, p, i, w, params, hashes, dev, normalize)
     return res
+
+
+def _resolve_lsh_ties(res: LshBatch, p, i, w, params: LshParams, hashes, dev,
+                      normalize: bool) -> None:
+    """Re-key the tables of sets whose darts had bit-identical ranks.
+
+    The fast path orders a bucket's equal ranks by fingerprint; the
+    reference orders them by index tuple (ref/annindex.py:77-81).  For the
+    (astronomically rare) flagged sets, materialise the darts at phi* on the
+    GPU, order each bucket by (rank, element, nu, rho, w, r, j), keep the K
+    smallest and fold them with mix64 (ref/annindex.py:135).
+    """
+    tied = torch.nonzero((res.status & DSK_STATUS_TIE) != 0).flatten()
+    if tied.numel() == 0:
+        return
+    L, K = params.L, params.K
+    rows = tied.cpu().numpy()
+    pp = p.cpu().numpy()
+    sub_ptr = np.zeros(rows.size + 1, dtype=np.int64)
+    np.cumsum(pp[rows + 1] - pp[rows], out=sub_ptr[1:])
+    take = torch.cat([torch.arange(int(pp[r]), int(pp[r + 1]), device=dev) for r in rows])
+    sub_ids = i[take]
+    wh = w[take].cpu().numpy()
+    l1 = np.empty(rows.size)
+    for s in range(rows.size):
+        seg = wh[sub_ptr[s]:sub_ptr[s + 1]]
+        if normalize:  # LshIndex: scale_pow2(-weight_class(l1)), ref/annindex.py:130-131
+            seg = np.ldexp(seg, -weight_class(float(np.sum(seg))))
+            wh[sub_ptr[s]:sub_ptr[s + 1]] = seg
+        l1[s] = float(np.sum(seg))
+    limits = res.phi[tied].cpu().numpy().astype(np.float64) / l1
+    offsets, status, cols = darts_batch(sub_ptr, sub_ids, wh, L * K, limits, hashes, device=dev)
+    fp = cols["fingerprint"]
+    h = _to_dev(hashes.hash64_array(as_u64(fp), stream=5, device=dev), torch.int64, dev)
+    hi = torch.bitwise_and(torch.bitwise_right_shift(h, 32), 0xFFFFFFFF)
+    lo = torch.bitwise_and(h, 0xFFFFFFFF)
+    bucket = ((hi % L) * (1 << 32) + lo) % L
+    owner = torch.repeat_interleave(torch.arange(rows.size, device=dev),
+                                    offsets[1:] - offsets[:-1])
+    flip = torch.tensor(-(2**63), dtype=torch.int64, device=dev)
+    keys = [cols["j"].to(torch.int64), cols["r"].to(torch.int64) & 0xFFFFFFFF,
+            cols["w"].to(torch.int64) & 0xFFFFFFFF, cols["rho"].to(torch.int64),
+            cols["nu"].to(torch.int64), cols["element"] ^ flip, cols["rank"], bucket, owner]
+    order = _lexsort_dev(keys)
+    sb = owner[order] * L + bucket[order]
+    first = torch.searchsorted(sb, sb, right=False)
+    pos = torch.arange(order.numel(), device=dev) - first
+    keep = pos < K
+    tab = torch.zeros((rows.size * L, K), dtype=torch.int64, device=dev)
+    tab[sb[keep], pos[keep]] = fp[order[keep]]
+    if res.fps is not None:
+        res.fps[tied] = tab.view(rows.size, L, K)
+    if res.keys is not None:
+        mixed = hashes.mix64_rows(as_u64(tab), device=dev)
+        res.keys[tied] = _to_dev(mixed, torch.int64, dev).view(rows.size, L)
+    res.status[tied] = res.status[tied] & 0xFF
 
 
 DART_COLUMNS = (("element", torch.int64), ("nu", torch.int16), ("rho", torch.int16),

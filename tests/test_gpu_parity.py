@@ -598,6 +598,30 @@ def test_tie_resolution_path():
     assert (res.status.cpu().numpy() == 0).all()
 
 
+@pytest.mark.parametrize("normalize", [False, True])
+def test_lsh_tie_resolution_path(normalize):
+    """LSH rows flagged DSK_STATUS_TIE are re-keyed by full index tuple on the
+    GPU (ref/annindex.py:77-81, :135); force the path on corrupted rows."""
+    from paper_2005_11547_b200 import api
+    indptr, ids, w = workloads.generate("cfg4", n=30, start=11)
+    f = fam(3)
+    params = LshParams(40, 5)
+    res = lsh_batch(indptr, ids, w, params, f, fps=True, normalize=normalize)
+    good_k, good_f = as_u64(res.keys).copy(), as_u64(res.fps).copy()
+    rows = torch.tensor([2, 9, 21], device=res.keys.device)
+    res.keys[rows] = 7
+    res.fps[rows] = 7
+    res.status[rows] = res.status[rows] | DSK_STATUS_TIE
+    dev = res.keys.device
+    p = torch.from_numpy(indptr).to(dev)
+    i = torch.from_numpy(ids.view(np.int64)).to(dev)
+    ww = torch.from_numpy(w).to(dev)
+    api._resolve_lsh_ties(res, p, i, ww, params, f, dev, normalize)
+    assert np.array_equal(as_u64(res.keys), good_k)
+    assert np.array_equal(as_u64(res.fps), good_f)
+    assert (res.status.cpu().numpy() == 0).all()
+
+
 # ------------------------------------------------- bottom-k and DSK1 (next rows)
 
 
