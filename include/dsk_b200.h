@@ -173,6 +173,18 @@ int dsk_exact_jaccard(const int64_t *a_ptr, const uint64_t *a_ids, const double 
                       const int64_t *pa, const int64_t *pb, int64_t npairs, double *out,
                       void *stream);
 
+/* bottom_k (ref/sketching.py:126-161) for each set of a CSR batch, fused:
+ * density t = k, the first phi step with >= k darts, the k smallest darts by
+ * (rank, element, nu, rho, w, r, j), ascending, as DartBatch columns of
+ * shape [n, k].  Per-set status as dsk_minhash_csr, plus DSK_SCRATCH when a
+ * set's darts outgrow the per-warp buffer (the caller recomputes it, e.g.
+ * with dsk_darts_csr). */
+int dsk_bottomk_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                    const double *weights, int64_t n, int32_t k, uint64_t *element, uint16_t *nu,
+                    uint16_t *rho, uint32_t *w, uint32_t *r, uint16_t *j, double *weight,
+                    double *rank, uint64_t *fingerprint, int32_t *status, int32_t *phi,
+                    void *stream);
+
 /* Number of kernels this library has launched in the process so far (all
  * entry points and contexts); a caller brackets a region with two reads. */
 uint64_t dsk_launch_count(void);

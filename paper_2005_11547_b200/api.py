@@ -671,15 +671,10 @@ class BottomKBatch:
     phi: torch.Tensor             # int32 [n]
 
 
-def bottom_k_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, device=None,
-                   check: bool = True) -> BottomKBatch:
-    """bottom_k for every CSR row (ref/sketching.py:146-156): density t = k;
-    at the first phi step with >= k darts, the k smallest by (rank, index)."""
-    k = int(k)
-    if k < 1:
-        raise ValidationError(f"k must be positive, got {k}")
-    dev = _device(device)
-    p, i, w = _csr_to_dev(indptr, ids, weights, dev)
+def _bottom_k_composed(p, i, w, k: int, hashes: HashFamily, dev, check: bool) -> BottomKBatch:
+    """bottom_k composed from the darts kernel (K6) and a device lexsort per
+    phi step; the fallback of the fused kernel (sets whose darts outgrow its
+    buffer, or k above its range)."""
     n = p.numel() - 1
     l1 = l1_batch(p, w, device=dev)
     cols = {name: torch.zeros((n, k), dtype=dt, device=dev) for name, dt in DART_COLUMNS}
@@ -720,6 +715,46 @@ def bottom_k_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, device=N
         pending = pending[~done & ~bad]
     if pending.numel():
         status[pending] = DSK_NOCONV
+    res = BottomKBatch(cols, status, phis)
+    if check:
+        raise_for_status(status)
+    return res
+
+
+_BOTTOMK_FUSED_MAX_K = 256  # counting-rank selection cost grows with k^2
+
+
+def bottom_k_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, device=None,
+                   check: bool = True) -> BottomKBatch:
+    """bottom_k for every CSR row (ref/sketching.py:146-156): density t = k;
+    at the first phi step with >= k darts, the k smallest by (rank, index).
+
+    k <= 256: one fused kernel (dsk_bottomk_csr); rows it cannot hold in its
+    buffer, and larger k, go through the composed darts + lexsort path."""
+    k = int(k)
+    if k < 1:
+        raise ValidationError(f"k must be positive, got {k}")
+    dev = _device(device)
+    p, i, w = _csr_to_dev(indptr, ids, weights, dev)
+    n = p.numel() - 1
+    if k > _BOTTOMK_FUSED_MAX_K:
+        return _bottom_k_composed(p, i, w, k, hashes, dev, check)
+    cols = {name: torch.zeros((n, k), dtype=dt, device=dev) for name, dt in DART_COLUMNS}
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    phis = torch.zeros(n, dtype=torch.int32, device=dev)
+    order = [cols[name] for name, _ in DART_COLUMNS]
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().dsk_bottomk_csr(
+            hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, k, *[_ptr(c) for c in order],
+            _ptr(status), _ptr(phis), _stream_ptr(dev)), "dsk_bottomk_csr")
+    spill = torch.nonzero(status == 7).flatten()  # DSK_SCRATCH: recompute those rows
+    if spill.numel():
+        sp, si, sw = _gather_rows(p, i, w, spill)
+        sub = _bottom_k_composed(sp, si, sw, k, hashes, dev, False)
+        for name, _ in DART_COLUMNS:
+            cols[name][spill] = sub.columns[name]
+        status[spill] = sub.status
+        phis[spill] = sub.phi
     res = BottomKBatch(cols, status, phis)
     if check:
         raise_for_status(status)

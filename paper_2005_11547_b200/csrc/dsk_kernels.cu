@@ -732,6 +732,8 @@ static size_t minhash_smem(int k, int G, int nw, bool global_slots = false) {
   return off_team(nw) + teams * kTeamCtlBytes + (global_slots ? 0 : (size_t)teams * k * 16);
 }
 
+static cudaError_t bottomk_set_smem(int bytes);  // dsk_bottomk.cuh
+
 extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const double *cdf_host,
                               const double *log2_thr_host, dsk_ctx **out) {
   if (!tables_host || !cdf_host || !log2_thr_host || !out) return set_err(DSK_EARG, "null argument");
@@ -766,6 +768,7 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(darts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
+  CUDA_TRY(bottomk_set_smem(smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1277,3 +1280,4 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
 
 #include "dsk_lsh_host.cuh"
 #include "dsk_extra.cuh"
+#include "dsk_bottomk.cuh"

@@ -722,6 +722,29 @@ def test_darts_and_bottom_k_large_sets_vs_oracle():
         assert np.array_equal(rk[s], od["rank"]), s
 
 
+def test_bottom_k_fused_spill_and_large_k_paths(monkeypatch):
+    """The fused bottom-k kernel, its DSK_SCRATCH fallback (forced with a
+    tiny buffer) and the composed path for k > 256 all equal the oracle."""
+    from paper_2005_11547_b200 import bottom_k_batch
+    indptr, ids, w = workloads.generate("cfg3", n=30, start=900)
+    orc = Oracle(2)
+    f = fam(2)
+    exp = {}
+    for k in (64, 300):
+        exp[k] = np.stack([orc.bottom_k(ids[indptr[s]:indptr[s + 1]],
+                                        w[indptr[s]:indptr[s + 1]], k)[2]["fingerprint"]
+                           for s in range(30)])
+    fused = as_u64(bottom_k_batch(indptr, ids, w, 64, f).columns["fingerprint"])
+    assert np.array_equal(fused, exp[64])
+    monkeypatch.setenv("DSK_BOTTOMK_CAP", "40")
+    spilled = bottom_k_batch(indptr, ids, w, 64, f)
+    assert np.array_equal(as_u64(spilled.columns["fingerprint"]), exp[64])
+    assert (spilled.status.cpu().numpy() == 0).all()
+    monkeypatch.delenv("DSK_BOTTOMK_CAP")
+    big = as_u64(bottom_k_batch(indptr, ids, w, 300, f).columns["fingerprint"])
+    assert np.array_equal(big, exp[300])
+
+
 def test_dsk1_records_byte_identical():
     from paper_2005_11547_b200 import (BottomKFingerprints, MinHashSketch, bottom_k_batch,
                                        dump_sketches, iter_sketches)
