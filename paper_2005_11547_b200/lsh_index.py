@@ -89,23 +89,29 @@ class LshIndex:
         sets = list(sets)
         if len(point_ids) != len(sets):
             raise ValueError("point_ids and sets differ in length")
-        seen = set()
-        for pid, x in zip(point_ids, sets):
-            if pid in self._pos or pid in seen:
-                raise ValidationError(f"duplicate point id {pid!r}")
-            if x.is_empty():
-                raise ValidationError("cannot index an empty set")
-            seen.add(pid)
         if not sets:
             return
+        lens = np.fromiter((x.l0 for x in sets), dtype=np.int64, count=len(sets))
+        new_ids = set(point_ids)
+        if len(new_ids) != len(point_ids) or not new_ids.isdisjoint(self._pos.keys()):
+            seen = set()
+            for pid in point_ids:  # report the first offender, as insert() would
+                if pid in self._pos or pid in seen:
+                    raise ValidationError(f"duplicate point id {pid!r}")
+                seen.add(pid)
+        if (lens == 0).any():
+            raise ValidationError("cannot index an empty set")
         dev = self.device
-        lens = np.array([x.l0 for x in sets], dtype=np.int64)
         indptr = np.zeros(lens.size + 1, dtype=np.int64)
         np.cumsum(lens, out=indptr[1:])
         ids = np.concatenate([x.ids for x in sets])
         w = np.concatenate([x.weights for x in sets])
         res = lsh_batch(indptr, ids, w, self.params, self.hashes, normalize=True, device=dev)
-        cls = torch.tensor([weight_class(x.l1) for x in sets], dtype=torch.int64, device=dev)
+        # weight classes (ref/annindex.py:39-44): frexp exponent - 1 of each l1
+        l1 = np.fromiter((x.l1 for x in sets), dtype=np.float64, count=len(sets))
+        if not (l1 > 0).all():
+            raise ValidationError("weight class requires a positive norm")
+        cls = torch.from_numpy(np.frexp(l1)[1].astype(np.int64) - 1).to(dev)
         p_new, i_new, w_new = _sorted_rows(_to_dev(indptr, torch.int64, dev),
                                            _to_dev(ids, torch.int64, dev),
                                            _to_dev(w, torch.float64, dev))
@@ -115,10 +121,10 @@ class LshIndex:
         self._w = torch.cat([self._w, w_new])
         self._cls = torch.cat([self._cls, cls])
         self._keys = torch.cat([self._keys, res.keys])
-        for pid, x in zip(point_ids, sets):
-            self._pos[pid] = len(self._ids)
-            self._ids.append(pid)
-            self._sets.append(x)
+        first = len(self._ids)
+        self._pos.update(zip(point_ids, range(first, first + len(point_ids))))
+        self._ids.extend(point_ids)
+        self._sets.extend(sets)
         if self._debug_keys is not None:
             keys = res.keys.cpu().numpy().view(np.uint64)
             for r, (pid, x) in enumerate(zip(point_ids, sets)):
