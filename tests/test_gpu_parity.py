@@ -730,12 +730,13 @@ def test_bottom_k_fused_spill_and_large_k_paths(monkeypatch):
     orc = Oracle(2)
     f = fam(2)
     exp = {}
-    for k in (64, 300):
+    for k in (64, 200, 256, 300):
         exp[k] = np.stack([orc.bottom_k(ids[indptr[s]:indptr[s + 1]],
                                         w[indptr[s]:indptr[s + 1]], k)[2]["fingerprint"]
                            for s in range(30)])
-    fused = as_u64(bottom_k_batch(indptr, ids, w, 64, f).columns["fingerprint"])
-    assert np.array_equal(fused, exp[64])
+    for k in (64, 200, 256):
+        fused = as_u64(bottom_k_batch(indptr, ids, w, k, f).columns["fingerprint"])
+        assert np.array_equal(fused, exp[k]), k
     monkeypatch.setenv("DSK_BOTTOMK_CAP", "40")
     spilled = bottom_k_batch(indptr, ids, w, 64, f)
     assert np.array_equal(as_u64(spilled.columns["fingerprint"]), exp[64])
