@@ -17,6 +17,7 @@ port of the reference on a bounded sample as the CPU baseline
   dsk1      DSK1 minhash records (ref/sketching.py:210-231), k = 256: the
             record kernel (GB/s against the HBM peak) and dump_sketches with
             the bytes on the host.
+  icws      the ICWS comparator (ref/baselines.py:84-161), cfg3 rows, k = 64.
 """
 
 from __future__ import annotations
@@ -263,16 +264,54 @@ def row_dsk1(dev):
             "cpu_gpu_bytes_identical": True}
 
 
+def row_icws(dev):
+    from oracle.oracle import Oracle
+    from paper_2005_11547_b200 import HashFamily, icws_batch, workloads
+    n, k = 100_000, 64
+    indptr, ids, w = workloads.generate("cfg3", n=n)
+    fam = HashFamily(2)
+    p, i, ww = _dev_csr(indptr, ids, w, dev)
+    ms = _events_ms(lambda: icws_batch(p, i, ww, k, fam, check=False))
+    # CPU: the reference's numpy formulation (ref/baselines.py:106-136) over
+    # the oracle's hash, one set at a time, single thread
+    orc = Oracle(2)
+    t0, rows = time.perf_counter(), 0
+    while time.perf_counter() - t0 < 5.0 and rows < n:
+        x_ids, x_w = ids[indptr[rows]:indptr[rows + 1]], w[indptr[rows]:indptr[rows + 1]]
+        m = x_ids.size
+        elem = np.broadcast_to(x_ids, (k, m))
+        coord = np.broadcast_to(np.arange(k, dtype=np.uint64)[:, None], (k, m))
+
+        def u(stream):
+            h = orc.hash64_array(elem, 0, 0, coord, 0, 0, stream)
+            return (h >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+        r = -(np.log1p(-u(6)) + np.log1p(-u(7)))
+        c = -(np.log1p(-u(8)) + np.log1p(-u(9)))
+        beta = u(10)
+        tick = np.floor(np.log(np.broadcast_to(x_w, (k, m))) / r + beta)
+        ln_a = np.log(c) - r * (tick - beta) - r
+        np.argmin(ln_a, axis=1)
+        rows += 1
+    cdt = time.perf_counter() - t0
+    return {"row": "ICWS comparator", "metric": "sketches/sec", "value": n / (ms / 1e3),
+            "unit": "sketches/sec", "ms_per_step": ms,
+            "config": {"workload": "cfg3 rows", "sets": n, "nnz": 64, "k": k},
+            "cpu_baseline": {"value": rows / cdt, "unit": "sketches/sec", "cores": 1,
+                             "kind": "port",
+                             "sample": f"first {rows} sets, numpy restatement, 1 thread"}}
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--row", default="all", choices=["all", "bottomk", "lshindex", "dsk1"])
+    ap.add_argument("--row", default="all", choices=["all", "bottomk", "lshindex", "dsk1", "icws"])
     args = ap.parse_args()
     import torch
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
-    rows = ["bottomk", "lshindex", "dsk1"] if args.row == "all" else [args.row]
+    rows = ["bottomk", "lshindex", "dsk1", "icws"] if args.row == "all" else [args.row]
     for r in rows:
-        res = {"bottomk": row_bottomk, "lshindex": row_lshindex, "dsk1": row_dsk1}[r](dev)
+        res = {"bottomk": row_bottomk, "lshindex": row_lshindex, "dsk1": row_dsk1,
+               "icws": row_icws}[r](dev)
         for line in (res if isinstance(res, list) else [res]):
             print(json.dumps(line), flush=True)
 

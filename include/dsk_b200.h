@@ -185,6 +185,14 @@ int dsk_bottomk_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
                     double *rank, uint64_t *fingerprint, int32_t *status, int32_t *phi,
                     void *stream);
 
+/* ICWS comparator (ref/baselines.py:84-161, the paper's Table 1 baseline):
+ * k consistent weighted samples (element id, tick) per set of a CSR batch.
+ * log / log1p come from CUDA's libdevice, so a sample can differ from the
+ * host reference's where two candidates tie to within an ulp. */
+int dsk_icws_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids, const double *weights,
+                 int64_t n, int32_t k, uint64_t *out_element, int64_t *out_tick, int32_t *status,
+                 void *stream);
+
 /* Number of kernels this library has launched in the process so far (all
  * entry points and contexts); a caller brackets a region with two reads. */
 uint64_t dsk_launch_count(void);

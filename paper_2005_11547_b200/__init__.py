@@ -11,6 +11,13 @@ from .constants import ValidationError, minhash_density
 from . import io, shard, workloads
 from .api import (
     DSK_STATUS_TIE,
+    IcwsBatch,
+    IcwsHashValue,
+    IcwsSketcher,
+    icws_batch,
+    icws_estimate_jaccard,
+    icws_fingerprints,
+    icws_minhash,
     BottomKBatch,
     BottomKFingerprints,
     BottomKSketch,
@@ -50,6 +57,8 @@ __all__ = [
     "make_weighted_set", "minhash_batch", "one_bit", "raise_for_status", "weight_class",
     "BottomKBatch", "BottomKFingerprints", "BottomKSketch", "bottom_k", "bottom_k_batch",
     "dump_sketch", "dump_sketches", "iter_sketches", "l1_batch", "load_sketch",
+    "IcwsBatch", "IcwsHashValue", "IcwsSketcher", "icws_batch", "icws_estimate_jaccard",
+    "icws_fingerprints", "icws_minhash",
 ]
 
 from .lsh_index import LshIndex, probe_classes  # noqa: E402

@@ -80,6 +80,7 @@ SIGNATURES = [
     ("dsk_ctx_device", ctypes.c_int, [_P]),
     ("dsk_minhash_density", _I64, [_I64]),
     ("dsk_launch_count", ctypes.c_uint64, []),
+    ("dsk_icws_csr", ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P]),
     ("dsk_bottomk_csr", ctypes.c_int,
      [_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P, _P]),
     ("dsk_h2d_bytes", ctypes.c_uint64, []),

@@ -999,3 +999,96 @@ __all__ = [
     "load_sketch",
 ]
 _ = dataclasses
+
+
+# ------------------------------------------------- ICWS comparator (f4)
+
+
+@dataclass(frozen=True)
+class IcwsHashValue:
+    """A consistent weighted sample: element id plus quantised log-weight tick
+    (ref/baselines.py:75-81)."""
+
+    element: int
+    tick: int
+
+
+@dataclass
+class IcwsBatch:
+    element: torch.Tensor  # int64 [n, k] (uint64 ids)
+    tick: torch.Tensor     # int64 [n, k]
+    status: torch.Tensor   # int32 [n]
+
+
+def icws_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, device=None,
+               check: bool = True) -> IcwsBatch:
+    """ICWS samples (ref/baselines.py:84-161) for every CSR row, on the GPU.
+
+    A comparator, not DartMinHash: log / log1p are CUDA's, so a sample may
+    differ from the host reference's where candidates tie to within an ulp
+    (none in the tested fixtures)."""
+    k = int(k)
+    if k < 1:
+        raise ValidationError(f"k must be positive, got {k}")
+    dev = _device(device)
+    p, i, w = _csr_to_dev(indptr, ids, weights, dev)
+    n = p.numel() - 1
+    el = torch.zeros((n, k), dtype=torch.int64, device=dev)
+    tk = torch.zeros((n, k), dtype=torch.int64, device=dev)
+    status = torch.zeros(n, dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().dsk_icws_csr(hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, k,
+                                            _ptr(el), _ptr(tk), _ptr(status), _stream_ptr(dev)),
+                   "dsk_icws_csr")
+    res = IcwsBatch(el, tk, status)
+    if check:
+        raise_for_status(status)
+    return res
+
+
+class IcwsSketcher:
+    """Ioffe consistent weighted sampling with HashFamily randomness
+    (ref/baselines.py:84-136); `fast` is accepted for API parity (the device
+    computes log(x) once per element either way; outputs are identical)."""
+
+    __slots__ = ("k", "hashes", "fast")
+
+    def __init__(self, k: int, hashes: HashFamily, fast: bool = False):
+        if k < 1:
+            raise ValidationError(f"k must be positive, got {k}")
+        self.k = k
+        self.hashes = hashes
+        self.fast = fast
+
+    @property
+    def seed(self) -> int:
+        return self.hashes.seed
+
+    def minhash(self, x: WeightedSet) -> list:
+        if x.is_empty():
+            raise ValidationError("cannot sketch an empty set")
+        res = icws_batch(*_single_csr(x), self.k, self.hashes)
+        el = as_u64(res.element[0])
+        tk = res.tick[0].cpu().numpy()
+        return [IcwsHashValue(int(e), int(t)) for e, t in zip(el, tk)]
+
+
+def icws_minhash(x: WeightedSet, k: int, hashes: HashFamily, fast: bool = False) -> list:
+    """k consistent weighted samples of x (ref/baselines.py:139-142)."""
+    return IcwsSketcher(k, hashes, fast=fast).minhash(x)
+
+
+def icws_estimate_jaccard(a: list, b: list) -> float:
+    """Fraction of coordinates whose samples collide (ref/baselines.py:145-149)."""
+    if len(a) != len(b):
+        raise ValidationError("sketch lengths differ")
+    return sum(u == v for u, v in zip(a, b)) / len(a)
+
+
+def icws_fingerprints(values: list, hashes: HashFamily) -> np.ndarray:
+    """64-bit fingerprints of ICWS samples (ref/baselines.py:152-161), on the GPU:
+    hash64(element, w = tick low 32 bits, r = tick high 32 bits, stream 11)."""
+    el = np.array([v.element & (2**64 - 1) for v in values], dtype=np.uint64)
+    tk = np.array([v.tick & (2**64 - 1) for v in values], dtype=np.uint64)
+    return hashes.hash64_array(el, w=tk & np.uint64(0xFFFFFFFF), r=tk >> np.uint64(32),
+                               stream=11)

@@ -1281,3 +1281,4 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
 #include "dsk_lsh_host.cuh"
 #include "dsk_extra.cuh"
 #include "dsk_bottomk.cuh"
+#include "dsk_icws.cuh"

@@ -873,3 +873,35 @@ def test_dart_count_is_poisson():
     assert (status.cpu().numpy() == 0).all()
     assert abs(counts.mean() - t) <= 4 * (t / sets) ** 0.5
     assert abs(counts.var() / t - 1.0) < 0.25
+
+
+# ------------------------------------------------------ ICWS comparator (f4)
+
+
+@pytest.mark.parametrize("k", [64, 200])
+def test_icws_matches_reference(k):
+    """ICWS samples and fingerprints against the reference's own outputs
+    (ref/baselines.py:84-161): cfg3 rows plus weights over 2^+-30."""
+    from paper_2005_11547_b200 import icws_batch, icws_fingerprints, IcwsHashValue
+    g = golden("icws.npz")
+    f = fam(int(g["seed"]))
+    res = icws_batch(g["indptr"], g["ids"], g["w"], k, f)
+    el = as_u64(res.element)
+    tk = res.tick.cpu().numpy()
+    mism = int(((el != g[f"element_k{k}"]) | (tk != g[f"tick_k{k}"])).sum())
+    assert mism == 0, f"{mism} of {el.size} samples differ (libm vs libdevice log)"
+    vals = [IcwsHashValue(int(e), int(t)) for e, t in zip(el[0], tk[0])]
+    assert np.array_equal(icws_fingerprints(vals, f), g[f"fp_k{k}"][0])
+
+
+def test_icws_api_semantics():
+    from paper_2005_11547_b200 import IcwsSketcher, icws_estimate_jaccard, icws_minhash
+    f = fam(9)
+    x = make_weighted_set([(1, 0.5), (2, 2.0), (7, 1.25)])
+    a = icws_minhash(x, 32, f)
+    assert a == IcwsSketcher(32, f, fast=True).minhash(x)
+    assert icws_estimate_jaccard(a, a) == 1.0
+    with pytest.raises(ValidationError):
+        icws_minhash(make_weighted_set([]), 8, f)
+    with pytest.raises(ValidationError):
+        IcwsSketcher(0, f)

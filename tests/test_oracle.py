@@ -188,3 +188,30 @@ def test_bottom_k_matches_reference():
             row = exp[s * k:(s + 1) * k]
             for name in row.dtype.names:
                 assert np.array_equal(darts[name], row[name]), (k, s, name)
+
+
+def test_icws_restatement_matches_reference():
+    """A numpy restatement of ICWS (ref/baselines.py:106-136) over the oracle's
+    hash reproduces the reference's golden samples (pins the comparator)."""
+    g = golden("icws.npz")
+    orc = Oracle(int(g["seed"]))
+    indptr, ids, w = g["indptr"], g["ids"], g["w"]
+    k = 64
+    for s in list(range(0, 120, 7)) + list(range(120, indptr.size - 1)):
+        x_ids, x_w = ids[indptr[s]:indptr[s + 1]], w[indptr[s]:indptr[s + 1]]
+        n = x_ids.size
+        elem = np.broadcast_to(x_ids, (k, n))
+        coord = np.broadcast_to(np.arange(k, dtype=np.uint64)[:, None], (k, n))
+
+        def u(stream):
+            h = orc.hash64_array(elem, 0, 0, coord, 0, 0, stream)
+            return (h >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+
+        r = -(np.log1p(-u(6)) + np.log1p(-u(7)))
+        c = -(np.log1p(-u(8)) + np.log1p(-u(9)))
+        beta = u(10)
+        tick = np.floor(np.log(np.broadcast_to(x_w, (k, n))) / r + beta)
+        ln_a = np.log(c) - r * (tick - beta) - r
+        win = np.argmin(ln_a, axis=1)
+        assert np.array_equal(x_ids[win], g["element_k64"][s]), s
+        assert np.array_equal(tick[np.arange(k), win].astype(np.int64), g["tick_k64"][s]), s
