@@ -15,8 +15,9 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "hi1": {},
-    "hi2": {"DSK_HIT_ILP": 2},
+    "f_def": {},
+    "f_dlcmcg": {},
+    "f_noexp": {},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
