@@ -1,6 +1,7 @@
 """Build tuning variants of libdsk_b200.so (in-tree, travel with gpurun) and
 time each on the quick workload list.  Variants are compile-time defines of
-csrc/dsk_engine.cuh (DSK_WARPS, DSK_RUN, DSK_DIRECT, DSK_REFILL).
+csrc/dsk_engine.cuh / dsk_kernels.cu / dsk_lsh_kernel.cuh (DSK_DIRECT,
+DSK_RUN, DSK_REFILL, DSK_FUSE, DSK_OPAQUE, DSK_LPT, DSK_LSH_CLOSE, ...).
 
   python profiles/sweep.py build            # here (nvcc, no GPU)
   python profiles/sweep.py run [workloads]  # on the GPU box
@@ -15,9 +16,13 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "f_def": {},
-    "f_dlcmcg": {},
-    "f_noexp": {},
+    # compile-time variants measured this round (DESIGN.md §9 lists the
+    # outcomes); the defaults of csrc/dsk_engine.cuh / dsk_kernels.cu won
+    "default": {},
+    "direct2": {"DSK_DIRECT": 2},
+    "refill12": {"DSK_REFILL": 12},
+    "no_opaque": {"DSK_OPAQUE": 0},
+    "no_lpt": {"DSK_LPT": 0},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
