@@ -125,6 +125,18 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
+def cpu_model() -> str:
+    """The host CPU's model string (BASELINE.md §2 asks for it next to the core count)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_baseline(cfg, k, indptr, ids, w, seconds, L=0, K=0):
     """The C oracle port of the reference on all host cores over a bounded sample."""
     from oracle.oracle import Oracle, default_threads
@@ -146,6 +158,7 @@ def cpu_baseline(cfg, k, indptr, ids, w, seconds, L=0, K=0):
     rows = int(min(n, max(probe, probe * seconds / max(dt, 1e-6))))
     dt = run(rows)
     return {"value": rows / dt, "unit": "sketches/sec", "cores": threads, "kind": "port",
+            "cpu_model": cpu_model(),
             "sample": f"first {rows} sets of the workload, {threads} threads, {dt:.1f} s"}
 
 
@@ -194,7 +207,7 @@ def reference_arm(args):
         "config": {"workload": cfg.name, "description": cfg.description, "k": k,
                    "sets_per_step": rows},
         "cpu_baseline": {"value": value, "unit": "sketches/sec", "cores": threads,
-                         "kind": "port",
+                         "kind": "port", "cpu_model": cpu_model(),
                          "sample": f"first {rows} sets of {cfg.name} per step, {threads} threads "
                                    "(C restatement of the reference, oracle/)"},
         "e2e": {"value": value, "unit": "sketches/sec", "h2d_bytes_per_step": 0,
