@@ -243,6 +243,23 @@ def test_lsh_max_sizes_vs_oracle():
     assert np.array_equal(res.phi.cpu().numpy(), phi)
 
 
+@pytest.mark.parametrize("cfg,k,rows", [("cfg2", 256, 100000), ("cfg3", 256, 100000),
+                                         ("cfg5", 128, 100000)])
+def test_minhash_full_size_vs_oracle(cfg, k, rows):
+    """Every slot of BASELINE-sized batches (cfg2 is its full 1e5 sets)
+    against the oracle: zero mismatching slots (north star: <= 1e-6)."""
+    _oracle_compare(cfg, k, rows)
+
+
+def test_lsh_large_batch_vs_oracle():
+    indptr, ids, w = workloads.generate("cfg4", n=30000, start=40000)
+    res = lsh_batch(indptr, ids, w, LshParams(100, 20), fam(3))
+    keys, _, status, phi, hits = Oracle(3).lsh_csr(indptr, ids, w, 100, 20)
+    assert (status == 0).all()
+    assert int((as_u64(res.keys) != keys).sum()) == 0
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+
+
 def test_minhash_cfg5_vs_oracle():
     _oracle_compare("cfg5", 128, 4000, start=200000)
 
