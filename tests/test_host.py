@@ -127,3 +127,23 @@ def test_no_cpu_path_without_cuda():
     f = HashFamily(1)
     with pytest.raises(RuntimeError, match="CUDA"):
         f.hash64(1)
+
+
+def test_bench_reference_arm_json_contract():
+    """`bench.py --impl reference` runs on the host alone and prints the
+    contract's JSON line (impl, metric, cpu_baseline, zero-copy e2e)."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run([sys.executable, os.path.join(repo, "bench.py"), "--impl", "reference",
+                          "--workload", "cfg1", "--steps", "1", "--warmup", "1"],
+                         capture_output=True, text=True, timeout=600, check=True).stdout
+    line = json.loads(out.strip().splitlines()[-1])
+    for key in ("impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step",
+                "higher_is_better", "cpu_baseline", "e2e", "config"):
+        assert key in line, key
+    assert line["impl"] == "reference" and line["metric"] == "sketches/sec"
+    assert line["value"] > 0 and line["higher_is_better"] is True
+    assert line["cpu_baseline"]["kind"] == "port" and line["cpu_baseline"]["cores"] >= 1
+    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
