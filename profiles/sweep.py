@@ -16,13 +16,8 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    # compile-time variants measured this round (DESIGN.md §9 lists the
-    # outcomes); the defaults of csrc/dsk_engine.cuh / dsk_kernels.cu won
-    "default": {},
-    "direct2": {"DSK_DIRECT": 2},
-    "refill12": {"DSK_REFILL": 12},
-    "no_opaque": {"DSK_OPAQUE": 0},
-    "no_lpt": {"DSK_LPT": 0},
+    "lfuse0": {},
+    "lfuse1": {"DSK_LSH_FUSE": 1},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
