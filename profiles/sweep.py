@@ -16,8 +16,9 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "lfuse0": {},
-    "lfuse1": {"DSK_LSH_FUSE": 1},
+    "fuse2": {},
+    "fuse1": {"DSK_FUSE": 1},
+    "fuse0": {"DSK_FUSE": 0},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
