@@ -33,6 +33,15 @@ def test_integration_stub_dart_minhash_many():
     sk = mod.dart_minhash_many(sets, 256, f)
     ref = as_u64(minhash_batch(indptr, ids, w, 256, f).values)
     assert np.array_equal(np.stack([s.values for s in sk]), ref)
+    # LshIndex-style keys (normalised) equal lsh_batch's
+    from paper_2005_11547_b200 import LshParams, lsh_batch
+    p4, i4, w4 = workloads.generate("cfg4", n=40)
+    sets4 = [dsk.WeightedSet.from_arrays(i4[p4[s]:p4[s + 1]], w4[p4[s]:p4[s + 1]])
+             for s in range(40)]
+    f4 = dsk.HashFamily(3)
+    keys = mod.lsh_keys_many(sets4, LshParams(100, 20), f4)
+    ref4 = as_u64(lsh_batch(p4, i4, w4, LshParams(100, 20), f4, normalize=True).keys)
+    assert np.array_equal(keys, ref4)
     # the stub's log2 thresholds equal the facade's
     from paper_2005_11547_b200.constants import log2_thresholds
     assert np.array_equal(mod._log2_thresholds(), log2_thresholds())
