@@ -26,7 +26,7 @@ NVCC_FLAGS = [
     "-O3", "-lineinfo", "-std=c++17",
     "-fmad=false",           # no DFMA contraction: the reference rounds every op
     "-Xptxas", "-v",
-    "-Xcompiler", "-fPIC", "-shared",
+    "-Xcompiler", "-fPIC,-fopenmp", "-shared", "-lgomp",
 ]
 
 _lock = threading.Lock()

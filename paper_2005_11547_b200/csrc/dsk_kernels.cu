@@ -19,6 +19,7 @@
 #include <string.h>
 
 #include <atomic>
+#include <thread>
 #include <mutex>
 #include <string>
 
@@ -57,6 +58,11 @@ struct dsk_ctx {
   size_t stage_bytes = 0;
   cudaStream_t hs[4] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t ev_in[kMaxChunks] = {}, ev_k[kMaxChunks] = {};
+  // pageable host inputs are staged through two pinned buffers (ids and
+  // weights of one chunk each), reused once their copy-out event fired
+  unsigned char *pin_stage[2] = {nullptr, nullptr};
+  size_t pin_bytes = 0;
+  cudaEvent_t ev_pin[2] = {nullptr, nullptr};
   // global scratch of the kernels (LSH hit buffers, large-k minhash slot
   // arrays): a small pool of slots reused in stream order, a launch waits for
   // the previous user of its slot (scratch_acquire / scratch_release)
@@ -799,6 +805,10 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
     if (c->ev_in[i]) cudaEventDestroy(c->ev_in[i]);
     if (c->ev_k[i]) cudaEventDestroy(c->ev_k[i]);
   }
+  for (int i = 0; i < 2; i++) {
+    if (c->pin_stage[i]) cudaFreeHost(c->pin_stage[i]);
+    if (c->ev_pin[i]) cudaEventDestroy(c->ev_pin[i]);
+  }
   delete c;
   return DSK_OK;
 }
@@ -1192,6 +1202,50 @@ extern "C" uint64_t dsk_h2d_bytes(void) { return g_h2d_bytes.load(); }
 // (Narrowing ids to u32 on the host before the copy was tried: 16 host
 // threads narrowing while the DMA engine reads the same host memory made the
 // cfg2 e2e step slower, 43.6 ms against 31.6 ms.)
+static bool is_pinned(const void *p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeHost;
+}
+
+// memcpy with the host's threads (pageable -> pinned staging)
+static void par_memcpy(void *dst, const void *src, size_t bytes, int threads) {
+  const int64_t blocks = (int64_t)threads * 4;
+  const size_t step = ((bytes + blocks - 1) / blocks + 63) & ~(size_t)63;
+#pragma omp parallel for num_threads(threads) schedule(static)
+  for (int64_t b = 0; b < blocks; b++) {
+    const size_t o = (size_t)b * step;
+    if (o < bytes) memcpy((char *)dst + o, (const char *)src + o, o + step < bytes ? step : bytes - o);
+  }
+}
+
+static int stage_threads() {
+  if (const char *e = getenv("DSK_HOST_THREADS")) return atoi(e) > 0 ? atoi(e) : 1;
+  unsigned hw = std::thread::hardware_concurrency();
+  return hw ? (int)(hw < 16 ? hw : 16) : 8;
+}
+
+static int ensure_pin_stage(dsk_ctx *c, size_t bytes) {
+  for (int b = 0; b < 2; b++)
+    if (!c->ev_pin[b]) {
+      CUDA_TRY(cudaEventCreateWithFlags(&c->ev_pin[b], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventRecord(c->ev_pin[b], c->hs[0]));
+    }
+  if (c->pin_bytes >= bytes) return DSK_OK;
+  CUDA_TRY(cudaStreamSynchronize(c->hs[0]));
+  for (int b = 0; b < 2; b++) {
+    if (c->pin_stage[b]) CUDA_TRY(cudaFreeHost(c->pin_stage[b]));
+    c->pin_stage[b] = nullptr;
+  }
+  c->pin_bytes = 0;
+  for (int b = 0; b < 2; b++) CUDA_TRY(cudaHostAlloc((void **)&c->pin_stage[b], bytes, 0));
+  c->pin_bytes = bytes;
+  return DSK_OK;
+}
+
 template <class Launch, class Out>
 static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                          const double *weights, int64_t n, int64_t *dp, uint64_t *di, double *dw,
@@ -1200,15 +1254,40 @@ static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
   int nch = 0;
   plan_chunks(indptr, n, host_chunk_cap(), bounds, kMaxChunks + 1, &nch);
   cudaStream_t cp = c->hs[0], os = c->hs[2];
+  // pageable inputs: stage each chunk through pinned buffers with the host's
+  // threads while the copy engine moves the previous chunk (a direct copy
+  // from pageable memory goes through the driver's own small bounce buffer
+  // and measured 6x slower on cfg2)
+  const bool stage = !(is_pinned(ids) && is_pinned(weights));
+  const int threads = stage_threads();
+  if (stage) {
+    int64_t mx = 0;
+    for (int ch = 0; ch < nch; ch++) {
+      int64_t m = indptr[bounds[ch + 1]] - indptr[bounds[ch]];
+      mx = m > mx ? m : mx;
+    }
+    int rc = ensure_pin_stage(c, (size_t)mx * 16);
+    if (rc) return rc;
+  }
   CUDA_TRY(cudaMemcpyAsync(dp, indptr, (n + 1) * 8, cudaMemcpyHostToDevice, cp));
   unsigned long long h2d = (unsigned long long)(n + 1) * 8;
   int rc = DSK_OK;
   for (int ch = 0; ch < nch && rc == DSK_OK; ch++) {
     const int64_t e0 = indptr[bounds[ch]], e1 = indptr[bounds[ch + 1]], m = e1 - e0;
-    CUDA_TRY(cudaMemcpyAsync(di + e0, ids + e0, m * 8, cudaMemcpyHostToDevice, cp));
-    h2d += (unsigned long long)m * 8;
-    CUDA_TRY(cudaMemcpyAsync(dw + e0, weights + e0, m * 8, cudaMemcpyHostToDevice, cp));
-    h2d += (unsigned long long)m * 8;
+    if (stage && m > 0) {
+      const int b = ch & 1;
+      CUDA_TRY(cudaEventSynchronize(c->ev_pin[b]));  // buffer b's previous copy is done
+      unsigned char *pb = c->pin_stage[b];
+      par_memcpy(pb, ids + e0, (size_t)m * 8, threads);
+      par_memcpy(pb + (size_t)m * 8, weights + e0, (size_t)m * 8, threads);
+      CUDA_TRY(cudaMemcpyAsync(di + e0, pb, m * 8, cudaMemcpyHostToDevice, cp));
+      CUDA_TRY(cudaMemcpyAsync(dw + e0, pb + (size_t)m * 8, m * 8, cudaMemcpyHostToDevice, cp));
+      CUDA_TRY(cudaEventRecord(c->ev_pin[b], cp));
+    } else {
+      CUDA_TRY(cudaMemcpyAsync(di + e0, ids + e0, m * 8, cudaMemcpyHostToDevice, cp));
+      CUDA_TRY(cudaMemcpyAsync(dw + e0, weights + e0, m * 8, cudaMemcpyHostToDevice, cp));
+    }
+    h2d += (unsigned long long)m * 16;
     CUDA_TRY(cudaEventRecord(c->ev_in[ch], cp));
     const int64_t r0 = bounds[ch], rows = bounds[ch + 1] - r0;
     cudaStream_t ks = c->hs[(compute_streams > 1 && (ch & 1)) ? 3 : 1];
