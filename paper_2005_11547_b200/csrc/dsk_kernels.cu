@@ -63,6 +63,12 @@ struct dsk_ctx {
   unsigned char *pin_stage[2] = {nullptr, nullptr};
   size_t pin_bytes = 0;
   cudaEvent_t ev_pin[2] = {nullptr, nullptr};
+  // pageable outputs: chunk results land in one of four pinned buffers and
+  // are copied out by the host threads four chunks later
+  static constexpr int kOutSlots = 4;
+  unsigned char *out_stage[kOutSlots] = {};
+  size_t out_bytes = 0;
+  cudaEvent_t ev_out[kOutSlots] = {};
   // global scratch of the kernels (LSH hit buffers, large-k minhash slot
   // arrays): a small pool of slots reused in stream order, a launch waits for
   // the previous user of its slot (scratch_acquire / scratch_release)
@@ -809,6 +815,10 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
     if (c->pin_stage[i]) cudaFreeHost(c->pin_stage[i]);
     if (c->ev_pin[i]) cudaEventDestroy(c->ev_pin[i]);
   }
+  for (int i = 0; i < dsk_ctx::kOutSlots; i++) {
+    if (c->out_stage[i]) cudaFreeHost(c->out_stage[i]);
+    if (c->ev_out[i]) cudaEventDestroy(c->ev_out[i]);
+  }
   delete c;
   return DSK_OK;
 }
@@ -1246,14 +1256,69 @@ static int ensure_pin_stage(dsk_ctx *c, size_t bytes) {
   return DSK_OK;
 }
 
+static int ensure_out_stage(dsk_ctx *c, size_t bytes) {
+  for (int b = 0; b < dsk_ctx::kOutSlots; b++)
+    if (!c->ev_out[b]) CUDA_TRY(cudaEventCreateWithFlags(&c->ev_out[b], cudaEventDisableTiming));
+  if (c->out_bytes >= bytes) return DSK_OK;
+  CUDA_TRY(cudaStreamSynchronize(c->hs[2]));
+  for (int b = 0; b < dsk_ctx::kOutSlots; b++) {
+    if (c->out_stage[b]) CUDA_TRY(cudaFreeHost(c->out_stage[b]));
+    c->out_stage[b] = nullptr;
+  }
+  c->out_bytes = 0;
+  for (int b = 0; b < dsk_ctx::kOutSlots; b++)
+    CUDA_TRY(cudaHostAlloc((void **)&c->out_stage[b], bytes, 0));
+  c->out_bytes = bytes;
+  return DSK_OK;
+}
+
+// Device-to-host copies of one chunk's results: straight into pinned
+// destinations, else into the chunk's pinned output slot, recorded for the
+// host threads to copy out once the slot's event fired.
+struct OutCopies {
+  struct Seg { void *dst; const void *src; size_t bytes; };
+  dsk_ctx *c;
+  int slot = 0;
+  size_t used = 0;
+  int nseg[dsk_ctx::kOutSlots] = {};
+  Seg seg[dsk_ctx::kOutSlots][8];
+  int operator()(void *dst, const void *src, size_t bytes, cudaStream_t st) {
+    if (bytes == 0) return DSK_OK;
+    if (is_pinned(dst) || nseg[slot] == 8 || used + bytes > c->out_bytes) {
+      CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+      return DSK_OK;
+    }
+    unsigned char *p = c->out_stage[slot] + used;
+    CUDA_TRY(cudaMemcpyAsync(p, src, bytes, cudaMemcpyDeviceToHost, st));
+    seg[slot][nseg[slot]++] = {dst, p, bytes};
+    used += (bytes + 255) & ~(size_t)255;
+    return DSK_OK;
+  }
+  int finish(int b, int threads) {  // copy slot b's results out to the caller
+    if (!nseg[b]) return DSK_OK;
+    CUDA_TRY(cudaEventSynchronize(c->ev_out[b]));
+    for (int i = 0; i < nseg[b]; i++) par_memcpy(seg[b][i].dst, seg[b][i].src, seg[b][i].bytes, threads);
+    nseg[b] = 0;
+    return DSK_OK;
+  }
+};
+
 template <class Launch, class Out>
 static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                          const double *weights, int64_t n, int64_t *dp, uint64_t *di, double *dw,
-                         int compute_streams, Launch launch, Out out) {
+                         int compute_streams, size_t out_row_bytes, Launch launch, Out out) {
   int64_t bounds[kMaxChunks + 1];
   int nch = 0;
   plan_chunks(indptr, n, host_chunk_cap(), bounds, kMaxChunks + 1, &nch);
   cudaStream_t cp = c->hs[0], os = c->hs[2];
+  OutCopies d2h;
+  d2h.c = c;
+  {
+    int64_t mx = 0;
+    for (int ch = 0; ch < nch; ch++) mx = bounds[ch + 1] - bounds[ch] > mx ? bounds[ch + 1] - bounds[ch] : mx;
+    int rc = ensure_out_stage(c, (size_t)mx * out_row_bytes + 8 * 256);
+    if (rc) return rc;
+  }
   // pageable inputs: stage each chunk through pinned buffers with the host's
   // threads while the copy engine moves the previous chunk (a direct copy
   // from pageable memory goes through the driver's own small bounce buffer
@@ -1296,9 +1361,20 @@ static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
     if (rc) break;
     CUDA_TRY(cudaEventRecord(c->ev_k[ch], ks));
     CUDA_TRY(cudaStreamWaitEvent(os, c->ev_k[ch], 0));
-    rc = out(r0, rows, os);
+    const int b = ch % dsk_ctx::kOutSlots;
+    rc = d2h.finish(b, threads);  // chunk ch - 4's results, if staged
+    if (rc) break;
+    d2h.slot = b;
+    d2h.used = 0;
+    rc = out(r0, rows, os, d2h);
+    if (rc) break;
+    CUDA_TRY(cudaEventRecord(c->ev_out[b], os));
   }
   for (int i = 0; i < 4; i++) CUDA_TRY(cudaStreamSynchronize(c->hs[i]));
+  for (int b = 0; b < dsk_ctx::kOutSlots; b++) {
+    int r2 = d2h.finish(b, threads);
+    if (!rc) rc = r2;
+  }
   g_h2d_bytes.fetch_add(h2d);
   return rc;
 }
@@ -1339,22 +1415,20 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
                            db ? db + r0 * words : nullptr, ds + r0, dph ? dph + r0 : nullptr,
                            dst ? dst + r0 * 4 : nullptr, st);
   };
-  auto out = [&](int64_t r0, int64_t m, cudaStream_t st) -> int {
-    if (out_values)
-      CUDA_TRY(cudaMemcpyAsync(out_values + r0 * k, dv + r0 * k, (size_t)m * k * 8,
-                               cudaMemcpyDeviceToHost, st));
-    if (out_bits)
-      CUDA_TRY(cudaMemcpyAsync(out_bits + r0 * words, db + r0 * words, (size_t)m * words * 8,
-                               cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(status + r0, ds + r0, m * 4, cudaMemcpyDeviceToHost, st));
-    if (phi) CUDA_TRY(cudaMemcpyAsync(phi + r0, dph + r0, m * 4, cudaMemcpyDeviceToHost, st));
-    if (stats)
-      CUDA_TRY(cudaMemcpyAsync(stats + r0 * 4, dst + r0 * 4, m * 16, cudaMemcpyDeviceToHost, st));
-    return DSK_OK;
+  auto out = [&](int64_t r0, int64_t m, cudaStream_t st, OutCopies &d2h) -> int {
+    int rc2 = DSK_OK;
+    if (out_values) rc2 |= d2h(out_values + r0 * k, dv + r0 * k, (size_t)m * k * 8, st);
+    if (out_bits) rc2 |= d2h(out_bits + r0 * words, db + r0 * words, (size_t)m * words * 8, st);
+    rc2 |= d2h(status + r0, ds + r0, (size_t)m * 4, st);
+    if (phi) rc2 |= d2h(phi + r0, dph + r0, (size_t)m * 4, st);
+    if (stats) rc2 |= d2h(stats + r0 * 4, dst + r0 * 4, (size_t)m * 16, st);
+    return rc2;
   };
   int streams = 2;
   if (const char *e = getenv("DSK_HOST_STREAMS")) streams = atoi(e) == 1 ? 1 : 2;
-  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, streams, launch, out);
+  const size_t row_bytes = (out_values ? (size_t)k * 8 : 0) + (out_bits ? (size_t)words * 8 : 0) +
+                           4 + (phi ? 4 : 0) + (stats ? 16 : 0);
+  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, streams, row_bytes, launch, out);
 }
 
 #include "dsk_lsh_host.cuh"

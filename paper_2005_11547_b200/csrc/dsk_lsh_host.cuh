@@ -104,18 +104,16 @@ extern "C" int dsk_lsh_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_
                        df ? df + r0 * L * K : nullptr, ds + r0, dph ? dph + r0 : nullptr,
                        dst ? dst + r0 * 4 : nullptr, st);
   };
-  auto out = [&](int64_t r0, int64_t m, cudaStream_t st) -> int {
-    if (out_keys)
-      CUDA_TRY(cudaMemcpyAsync(out_keys + r0 * L, dk + r0 * L, (size_t)m * L * 8,
-                               cudaMemcpyDeviceToHost, st));
-    if (out_fps)
-      CUDA_TRY(cudaMemcpyAsync(out_fps + r0 * L * K, df + r0 * L * K, (size_t)m * L * K * 8,
-                               cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(status + r0, ds + r0, m * 4, cudaMemcpyDeviceToHost, st));
-    if (phi) CUDA_TRY(cudaMemcpyAsync(phi + r0, dph + r0, m * 4, cudaMemcpyDeviceToHost, st));
-    if (stats)
-      CUDA_TRY(cudaMemcpyAsync(stats + r0 * 4, dst + r0 * 4, m * 16, cudaMemcpyDeviceToHost, st));
-    return DSK_OK;
+  auto out = [&](int64_t r0, int64_t m, cudaStream_t st, OutCopies &d2h) -> int {
+    int rc2 = DSK_OK;
+    if (out_keys) rc2 |= d2h(out_keys + r0 * L, dk + r0 * L, (size_t)m * L * 8, st);
+    if (out_fps) rc2 |= d2h(out_fps + r0 * L * K, df + r0 * L * K, (size_t)m * L * K * 8, st);
+    rc2 |= d2h(status + r0, ds + r0, (size_t)m * 4, st);
+    if (phi) rc2 |= d2h(phi + r0, dph + r0, (size_t)m * 4, st);
+    if (stats) rc2 |= d2h(stats + r0 * 4, dst + r0 * 4, (size_t)m * 16, st);
+    return rc2;
   };
-  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, 2, launch, out);
+  const size_t row_bytes = (out_keys ? (size_t)L * 8 : 0) + (out_fps ? (size_t)L * K * 8 : 0) +
+                           4 + (phi ? 4 : 0) + (stats ? 16 : 0);
+  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, 2, row_bytes, launch, out);
 }

@@ -12,8 +12,14 @@ ctx = fam.context(torch.device("cuda", 0))
 P = ctypes.c_void_p
 n, k = indptr.size - 1, 256
 res = {}
-for name in ("pageable", "pinned"):
-    if name == "pinned":
+for name in ("pageable", "pinned", "pinned_in_pageable_out"):
+    if name == "pinned_in_pageable_out":
+        ip = torch.from_numpy(indptr).pin_memory().numpy()
+        ii = torch.from_numpy(ids.view(np.int64)).pin_memory().numpy().view(np.uint64)
+        ww = torch.from_numpy(w).pin_memory().numpy()
+        vals = np.empty((n, k), dtype=np.int64)
+        st = np.empty(n, dtype=np.int32)
+    elif name == "pinned":
         ip = torch.from_numpy(indptr).pin_memory().numpy()
         ii = torch.from_numpy(ids.view(np.int64)).pin_memory().numpy().view(np.uint64)
         ww = torch.from_numpy(w).pin_memory().numpy()
