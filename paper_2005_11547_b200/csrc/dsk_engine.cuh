@@ -50,7 +50,7 @@ namespace dsk {
 #define DSK_WARPS 24
 #endif
 #ifndef DSK_RUN
-#define DSK_RUN 4
+#define DSK_RUN 3
 #endif
 #ifndef DSK_DIRECT
 #define DSK_DIRECT 1  // 0: off, 1: only when the rank depth is 0, 2: always when tables fit

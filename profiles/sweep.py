@@ -16,9 +16,10 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "fuse2": {},
-    "fuse1": {"DSK_FUSE": 1},
-    "fuse0": {"DSK_FUSE": 0},
+    "run4": {},
+    "run2": {"DSK_RUN": 2},
+    "run6": {"DSK_RUN": 6},
+    "run3": {"DSK_RUN": 3},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
