@@ -16,10 +16,10 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "run4": {},
-    "run2": {"DSK_RUN": 2},
-    "run6": {"DSK_RUN": 6},
-    "run3": {"DSK_RUN": 3},
+    "rf8": {},
+    "rf6": {"DSK_REFILL": 6},
+    "rf10": {"DSK_REFILL": 10},
+    "rf12": {"DSK_REFILL": 12},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]

@@ -550,6 +550,35 @@ def test_lsh_host_buffer_abi():
     assert np.array_equal(keys, as_u64(dev.keys))
 
 
+def test_host_buffer_pinned_and_pageable_mixes():
+    """dsk_minhash_csr_host with pinned inputs/outputs (direct DMA), pageable
+    ones (staged through the context's pinned buffers) and mixes of both."""
+    import ctypes
+
+    from paper_2005_11547_b200 import _lib
+    indptr, ids, w = workloads.generate("cfg2", n=3000, start=321)
+    f = fam(1)
+    ref = as_u64(minhash_batch(indptr, ids, w, 256, f).values)
+    P = lambda a: ctypes.c_void_p(a.ctypes.data)  # noqa: E731
+
+    def pinned(a):
+        t = torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).pin_memory()
+        out = t.numpy()
+        return out.view(np.uint64) if a.dtype == np.uint64 else out
+
+    for pin_in in (False, True):
+        for pin_out in (False, True):
+            ii = pinned(ids) if pin_in else ids
+            ww = pinned(w) if pin_in else w
+            vals = pinned(np.zeros((3000, 256), np.uint64)) if pin_out else \
+                np.zeros((3000, 256), np.uint64)
+            st = pinned(np.zeros(3000, np.int32)) if pin_out else np.zeros(3000, np.int32)
+            rc = _lib.load().dsk_minhash_csr_host(f.context(), P(indptr), P(ii), P(ww), 3000, 256,
+                                                 P(vals), None, P(st), None, None)
+            assert rc == 0 and (st == 0).all()
+            assert np.array_equal(vals, ref), (pin_in, pin_out)
+
+
 @pytest.mark.parametrize("chunk_mb", ["1", "3"])
 def test_host_pipeline_many_chunks(monkeypatch, chunk_mb):
     """Small chunk caps: many chunks through the three-stream pipeline (input
