@@ -1316,7 +1316,10 @@ static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
   {
     int64_t mx = 0;
     for (int ch = 0; ch < nch; ch++) mx = bounds[ch + 1] - bounds[ch] > mx ? bounds[ch + 1] - bounds[ch] : mx;
-    int rc = ensure_out_stage(c, (size_t)mx * out_row_bytes + 8 * 256);
+    // (at most 256 MB per slot: larger chunk outputs fall back to direct copies)
+    size_t want = (size_t)mx * out_row_bytes + 8 * 256;
+    if (want > ((size_t)256 << 20)) want = (size_t)256 << 20;
+    int rc = ensure_out_stage(c, want);
     if (rc) return rc;
   }
   // pageable inputs: stage each chunk through pinned buffers with the host's
