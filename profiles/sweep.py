@@ -16,10 +16,15 @@ sys.path.insert(0, REPO)
 VDIR = os.path.join(REPO, "paper_2005_11547_b200", "variants")
 
 VARIANTS = {
-    "rf8": {},
-    "rf6": {"DSK_REFILL": 6},
-    "rf10": {"DSK_REFILL": 10},
-    "rf12": {"DSK_REFILL": 12},
+    # compile-time variants measured this round (DESIGN.md §9 lists the
+    # outcomes); the defaults of csrc/dsk_engine.cuh / dsk_kernels.cu won
+    "default": {},
+    "direct2": {"DSK_DIRECT": 2},
+    "run4": {"DSK_RUN": 4},
+    "refill12": {"DSK_REFILL": 12},
+    "no_opaque": {"DSK_OPAQUE": 0},
+    "no_lpt": {"DSK_LPT": 0},
+    "lsh_nofuse": {"DSK_LSH_FUSE": 0},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
