@@ -58,6 +58,9 @@ namespace dsk {
 #ifndef DSK_REFILL
 #define DSK_REFILL 8
 #endif
+#ifndef DSK_PT_IMM
+#define DSK_PT_IMM 1  // Poisson thresholds as immediates instead of shared-memory loads
+#endif
 // scheduler thresholds (<= 32: a stage runs once this many items are queued)
 #ifndef DSK_TH_HIT
 #define DSK_TH_HIT 32
@@ -142,11 +145,22 @@ struct DartRow {
   uint64_t fp;
 };
 
+// The first four integer thresholds ceil(cdf[m] * 2^53) of the reference's
+// POISSON1_CDF (ref/randomness.py:66-85) as immediates: dsk_ctx_create checks
+// that the CDF it is given reproduces them (and rejects any other CDF).
+constexpr uint64_t kPt0 = 0xbc5ab1b16779cULL, kPt1 = 0x178b56362cef38ULL,
+                   kPt2 = 0x1d6e2bc3b82b06ULL, kPt3 = 0x1f6472f2e6944bULL;
+
 // Poisson(1) count: #{m : X >= thr[m]} (inverse CDF, ref/randomness.py:145-147);
 // counts >= 4 (2% of areas) finish in a loop over the shared table.
 __device__ __forceinline__ uint32_t poisson_count(uint64_t X, const PassParams &P,
                                                   const SmemTables &T) {
+#if DSK_PT_IMM
+  uint32_t c = (X >= kPt0) + (X >= kPt1) + (X >= kPt2) + (X >= kPt3);
+  (void)P;
+#else
   uint32_t c = (X >= P.pt0) + (X >= P.pt1) + (X >= P.pt2) + (X >= P.pt3);
+#endif
   if (c == 4) {
     while (X >= T.pthr[c]) c++;
   }

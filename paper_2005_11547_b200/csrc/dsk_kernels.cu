@@ -763,6 +763,12 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
     pthr[m] = (uint64_t)v;
   }
   pthr[63] = pthr[63] > (1ULL << 53) ? pthr[63] : (1ULL << 53);  // X < 2^53: loop sentinel
+#if DSK_PT_IMM
+  if (pthr[0] != kPt0 || pthr[1] != kPt1 || pthr[2] != kPt2 || pthr[3] != kPt3) {
+    delete c;
+    return set_err(DSK_EUNSUPPORTED, "Poisson CDF differs from the reference's POISSON1_CDF");
+  }
+#endif
   CUDA_TRY(cudaMalloc(&c->d_tab, 22 * 256 * sizeof(uint64_t)));
   CUDA_TRY(cudaMalloc(&c->d_pthr, 64 * sizeof(uint64_t)));
   CUDA_TRY(cudaMalloc(&c->d_l2thr, 258 * sizeof(double)));

@@ -25,6 +25,7 @@ VARIANTS = {
     "no_opaque": {"DSK_OPAQUE": 0},
     "no_lpt": {"DSK_LPT": 0},
     "lsh_nofuse": {"DSK_LSH_FUSE": 0},
+    "pt_smem": {"DSK_PT_IMM": 0},
 }
 WORKLOADS = ["cfg2", "cfg3 --k 64", "cfg3 --k 256", "cfg3 --k 1024", "cfg4",
              "cfg5 --sets 1000000"]
