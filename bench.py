@@ -1,23 +1,43 @@
 """Benchmark: DartMinHash sketching throughput on B200 (BASELINE.json metric).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg2]
-    python bench.py --impl reference ...      # CPU reference arm (oracle port)
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4]
+    python bench.py --impl reference ...      # CPU reference arm
 
-A step = one pass of the hot path (dart_minhash for every set; lsh keys for
-cfg4) over one batch of the workload, inputs resident in HBM.  Default
-workload = BASELINE configs[1] (cfg2: 1e5 sets, nnz 1024, k 256), which fits
-one GPU.  Under torchrun each rank sketches its own 1e5-set row block (weak
-scaling, no data-path collective: the sets are independent).
+A step = one pass of the hot path over one batch of the workload with the
+inputs resident in HBM: `lsh_batch` (ref/annindex.py:64-82 + mix64 per table)
+for cfg4, `minhash_batch` (ref/sketching.py:115-123, + the 1-bit epilogue for
+cfg3) otherwise.  The default workload is cfg4 (BASELINE configs[3]: 1e6 sets,
+nnz 128, LogNormal(0,1), (L,K) = (100,20)), the largest configuration whose
+sets fit one GPU per the round-1 verdict; cfg1-cfg5 are all selectable, cfg5
+at its full 1e7 sets.
+
+Under torchrun (one rank per GPU) the batch is the SAME n sets for every N
+(strong scaling): the row ranges come from `shard.plan_shards_lengths` over
+the workload's row lengths (computed without generating the rows), each rank
+generates and sketches only its own range, and there is no data-path
+collective (the sets are independent).  The timed region is
+bracketed by barrier + synchronize; the time is the max over ranks.
 
 Prints ONE JSON line (rank 0).  Extra keys:
-  roofline      ALU bound: algorithmic hash evaluations (A + 2D + 2H per set,
-                SURVEY.md §8(d)) per second vs the K0 peak hash rate measured
-                in the same run; roofline_hbm gives the HBM view and
-                roofline_issue the warp-instruction issue rate (the resource
-                the kernel is actually bound by, ~65 % busy per ncu).
-  cpu_baseline  the C oracle port of the reference on the host's cores.
-  e2e           the same metric through the C ABI with host buffers
-                (dsk_minhash_csr_host), H2D + D2H inside the timed region.
+  roofline          the binding resource, warp-instruction issue: ncu's
+                    instruction count per set for this workload
+                    (profiles/ncu_traffic.json, same command captured under
+                    ncu) x sets / kernel time, against 4 issues/clk/SM at the
+                    SM clock sampled during the timed region; `traffic` = the
+                    same capture's DRAM bytes scaled to this launch.
+  roofline_useful   the useful-work lower bound: the areas, candidate darts,
+                    hits (and mix64 steps) of this step, each priced at the
+                    rate the K0 unit microbenchmarks reach on this GPU in this
+                    run with no enumeration bookkeeping; frac = that time /
+                    the kernel time.
+  roofline_hbm      CSR bytes + outputs over the measured copy bandwidth.
+  cpu_baseline      the unmodified Python reference (baseline/_ref) on every
+                    host core (multiprocessing) over a bounded
+                    sample; `cpu_port` = the C restatement (oracle/) likewise.
+  e2e               the same metric through the C ABI with host buffers
+                    (dsk_lsh_csr_host / dsk_minhash_csr_host), H2D + D2H in the
+                    timed region, pinned buffers; `e2e_pageable` = the same call
+                    with plain numpy arrays (the INTEGRATION.md binding).
 """
 
 from __future__ import annotations
@@ -46,12 +66,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--workload", default="cfg2")
+    ap.add_argument("--workload", default="cfg4")
     ap.add_argument("--k", type=int, default=None, help="slot count (cfg3: 64/256/1024)")
-    ap.add_argument("--sets", type=int, default=None, help="override sets per rank")
+    ap.add_argument("--sets", type=int, default=None, help="override the workload's set count")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
     return ap.parse_args()
 
 
@@ -59,19 +79,39 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    return rank, world, local
+    local_world = int(os.environ.get("LOCAL_WORLD_SIZE", str(world)))
+    return rank, world, local, local_world
 
 
-def workload_rows(cfg, rank, n_per_rank):
-    """CSR rows of this rank (optionally cached as .npy under $DSK_WL_CACHE)."""
+def host_cores() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def density(cfg, k):
+    from paper_2005_11547_b200.constants import minhash_density
+    return cfg.L * cfg.K if cfg.kind == "lsh" else minhash_density(k)
+
+
+def shard_bounds(cfg, n_total, world, k):
+    """Row ranges of the ranks: balanced by the per-row cost model over the
+    workload's row lengths (drawn without generating the rows)."""
+    from paper_2005_11547_b200 import shard, workloads
+    lens = workloads.lengths(cfg.name, n_total)
+    return shard.plan_shards_lengths(lens, world, density(cfg, k))
+
+
+def rows_of(cfg, r0, r1, workers):
+    """CSR rows [r0, r1) of the workload (optionally cached under $DSK_WL_CACHE)."""
     from paper_2005_11547_b200 import workloads
     cache = os.environ.get("DSK_WL_CACHE")
-    if cache:
-        base = os.path.join(cache, f"{cfg.name}_{rank * n_per_rank}_{n_per_rank}")
-        if os.path.exists(base + "_w.npy"):
-            return (np.load(base + "_p.npy"), np.load(base + "_i.npy"), np.load(base + "_w.npy"))
-    out = workloads.generate(cfg.name, n=n_per_rank, start=rank * n_per_rank)
-    if cache:
+    base = os.path.join(cache, f"{cfg.name}_{r0}_{r1 - r0}") if cache else None
+    if base and os.path.exists(base + "_w.npy"):
+        return (np.load(base + "_p.npy"), np.load(base + "_i.npy"), np.load(base + "_w.npy"))
+    out = workloads.generate(cfg.name, n=r1 - r0, start=r0, workers=workers)
+    if base:
         os.makedirs(cache, exist_ok=True)
         for suffix, arr in zip(("_p", "_i", "_w"), out):
             np.save(base + suffix + ".npy", arr)
@@ -125,21 +165,13 @@ class ClockSampler:
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
-def cpu_model() -> str:
-    """The host CPU's model string (BASELINE.md §2 asks for it next to the core count)."""
-    try:
-        for line in open("/proc/cpuinfo"):
-            if line.startswith("model name"):
-                return line.split(":", 1)[1].strip()
-    except OSError:
-        pass
-    import platform
-    return platform.processor() or "unknown"
+# ------------------------------------------------------------ CPU baselines
 
-
-def cpu_baseline(cfg, k, indptr, ids, w, seconds, L=0, K=0):
-    """The C oracle port of the reference on all host cores over a bounded sample."""
+def cpu_port(cfg, k, indptr, ids, w, seconds):
+    """The C restatement of the reference (oracle/, test infrastructure) on
+    all host threads over a bounded sample of the same rows."""
     from oracle.oracle import Oracle, default_threads
+    from baseline.pyref import cpu_model
     orc = Oracle(cfg.seed)
     threads = default_threads()
     n = indptr.size - 1
@@ -148,7 +180,7 @@ def cpu_baseline(cfg, k, indptr, ids, w, seconds, L=0, K=0):
         sub = (indptr[:rows + 1], ids[:indptr[rows]], w[:indptr[rows]])
         t0 = time.perf_counter()
         if cfg.kind == "lsh":
-            orc.lsh_csr(*sub, L, K, nthreads=threads)
+            orc.lsh_csr(*sub, cfg.L, cfg.K, nthreads=threads)
         else:
             orc.minhash_csr(*sub, k, nthreads=threads)
         return time.perf_counter() - t0
@@ -159,61 +191,127 @@ def cpu_baseline(cfg, k, indptr, ids, w, seconds, L=0, K=0):
     dt = run(rows)
     return {"value": rows / dt, "unit": "sketches/sec", "cores": threads, "kind": "port",
             "cpu_model": cpu_model(),
-            "sample": f"first {rows} sets of the workload, {threads} threads, {dt:.1f} s"}
+            "sample": f"first {rows} sets of {cfg.name} (this rank's rows), {threads} threads, "
+                      f"{dt:.1f} s"}
+
+
+def cpu_reference(cfg, k, indptr, ids, w, seconds, pool=None):
+    """The unmodified Python reference on every host core (baseline/pyref.py)."""
+    from baseline import pyref
+    if not pyref.available():
+        return None
+    own = pool is None
+    pool = pool or pyref.PyRefPool()
+    try:
+        rate, rows, _ = pool.timed_sample(cfg.kind, cfg.seed, k, cfg.L, cfg.K, cfg.onebit,
+                                          indptr, ids, w, seconds)
+    finally:
+        if own:
+            pool.close()
+    call = ("lsh_key + mix64 per table" if cfg.kind == "lsh" else
+            "dart_minhash" + (" + one_bit" if cfg.onebit else ""))
+    return {"value": rate, "unit": "sketches/sec", "cores": pool.workers, "kind": "reference",
+            "cpu_model": pyref.cpu_model(),
+            "sample": f"first {rows} sets of {cfg.name}, unmodified dartsketch 0.1.0 "
+                      f"({call}), {pool.workers} processes, ~{seconds:.0f} s busy each"}
 
 
 def reference_arm(args):
-    """--impl reference: the oracle port (C restatement of the reference) on CPU."""
-    rank, world, _ = dist_env()
+    """--impl reference: the reference's own CPU implementation of the path on
+    the host's cores -- the unmodified Python package (baseline/_ref) when it
+    is installed, else the C restatement (oracle/) -- over a bounded sample of
+    the workload per step.  Rank 0 only."""
+    rank, world, _, _ = dist_env()
     if rank != 0:
         return
+    from baseline import pyref
     from paper_2005_11547_b200 import workloads
-    from oracle.oracle import Oracle, default_threads
     cfg = workloads.CONFIGS[args.workload]
     k = args.k or (cfg.k[0] if cfg.k else 0)
-    threads = default_threads()
-    orc = Oracle(cfg.seed)
-    # bounded sample per step: ~args.cpu_seconds/steps of CPU work
-    n_avail = min(cfg.n, 20000)
+    n_avail = min(args.sets or cfg.n, 20000)
     indptr, ids, w = workloads.generate(cfg.name, n=n_avail)
+    per_step = max(2.0, 90.0 / max(1, args.steps + args.warmup))
+    port = cpu_port(cfg, k, indptr, ids, w, min(per_step, 5.0))
+    if pyref.available():
+        pool = pyref.PyRefPool()
+        probe = min(n_avail, 2 * pool.workers)
+        rate, _ = pool.run(cfg.kind, cfg.seed, k, cfg.L, cfg.K, cfg.onebit, indptr, ids, w, probe)
+        rows = int(min(n_avail, max(probe, rate * per_step)))
+        run = lambda m: pool.run(cfg.kind, cfg.seed, k, cfg.L, cfg.K, cfg.onebit,  # noqa: E731
+                                 indptr, ids, w, m)[0]
+        kind, cores = "reference", pool.workers
+        sample = (f"first {rows} sets of {cfg.name} per step, unmodified dartsketch 0.1.0 "
+                  f"(baseline/_ref), {cores} processes")
+    else:
+        from oracle.oracle import Oracle, default_threads
+        orc = Oracle(cfg.seed)
+        cores = default_threads()
+        pool = None
 
-    def step(rows):
-        sub = (indptr[:rows + 1], ids[:indptr[rows]], w[:indptr[rows]])
-        if cfg.kind == "lsh":
-            orc.lsh_csr(*sub, cfg.L, cfg.K, nthreads=threads)
-        else:
-            orc.minhash_csr(*sub, k, nthreads=threads)
-
-    probe = min(n_avail, threads * 8)
-    t0 = time.perf_counter()
-    step(probe)
-    dt = time.perf_counter() - t0
-    per_step = max(2.0, 60.0 / max(1, args.steps + args.warmup))
-    rows = int(min(n_avail, max(probe, probe * per_step / max(dt, 1e-6))))
+        def run(m):
+            sub = (indptr[:m + 1], ids[:indptr[m]], w[:indptr[m]])
+            t0 = time.perf_counter()
+            if cfg.kind == "lsh":
+                orc.lsh_csr(*sub, cfg.L, cfg.K, nthreads=cores)
+            else:
+                orc.minhash_csr(*sub, k, nthreads=cores)
+            return m / (time.perf_counter() - t0)
+        rows = int(min(n_avail, port["value"] * per_step))
+        kind = "port"
+        sample = f"first {rows} sets of {cfg.name} per step, {cores} threads (C restatement, oracle/)"
     for _ in range(args.warmup):
-        step(min(rows, probe))
-    times = []
-    for _ in range(args.steps):
-        t0 = time.perf_counter()
-        step(rows)
-        times.append(time.perf_counter() - t0)
-    ms = 1000.0 * sum(times) / len(times)
+        run(min(rows, 2 * cores))
+    rates = [run(rows) for _ in range(args.steps)]
+    if pool is not None:
+        pool.close()
+    ms = 1000.0 * statistics.mean(rows / r for r in rates)
     value = rows / (ms / 1000.0)
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "sketches/sec",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64/f64",
-        "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u64/f64", "data": "synthetic",
         "config": {"workload": cfg.name, "description": cfg.description, "k": k,
-                   "sets_per_step": rows},
-        "cpu_baseline": {"value": value, "unit": "sketches/sec", "cores": threads,
-                         "kind": "port", "cpu_model": cpu_model(),
-                         "sample": f"first {rows} sets of {cfg.name} per step, {threads} threads "
-                                   "(C restatement of the reference, oracle/)"},
+                   "L": cfg.L or None, "K": cfg.K or None, "sets_per_step": rows},
+        "cpu_baseline": {"value": value, "unit": "sketches/sec", "cores": cores, "kind": kind,
+                         "cpu_model": pyref.cpu_model(), "sample": sample},
+        "cpu_port": port,
         "e2e": {"value": value, "unit": "sketches/sec", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ GPU arm
+
+def unit_rates(lib, ctx, dev, stream):
+    """K0 microbenchmarks (units/s on this GPU): 0 reference hash, 1 hoisted
+    hash, 2 area, 3 candidate dart, 4 hit, 5 mix64 step."""
+    import torch
+    sink = torch.zeros(1, dtype=torch.int64, device=dev)
+    iters = {0: 256, 1: 4096, 2: 2048, 3: 2048, 4: 1024, 5: 1024}
+    rates = {}
+    for mode, it in iters.items():
+        done = ctypes.c_int64()
+        lib.dsk_hash_peak(ctx, mode, 16, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(done),
+                          stream)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lib.dsk_hash_peak(ctx, mode, it, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(done),
+                          stream)
+        e1.record()
+        torch.cuda.synchronize()
+        rates[mode] = done.value / (e0.elapsed_time(e1) / 1000.0)
+    return rates
+
+
+def ncu_entry(cfg, k, explicit_k):
+    path = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    key = cfg.name if not explicit_k else f"{cfg.name}_k{k}"
+    return json.load(open(path)).get(key)
 
 
 def main():
@@ -221,13 +319,24 @@ def main():
     if args.impl == "reference":
         reference_arm(args)
         return
+    from paper_2005_11547_b200 import workloads
+    rank, world, local, local_world = dist_env()
+    cfg = workloads.CONFIGS[args.workload]
+    k = args.k or (cfg.k[0] if cfg.k else 0)
+    n_total = args.sets or cfg.n
+    # shard plan + this rank's rows, before CUDA is touched (the generator
+    # forks host workers); the ranks of a node share its cores
+    bounds = shard_bounds(cfg, n_total, world, k)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    t_gen = time.perf_counter()
+    indptr, ids, w = rows_of(cfg, r0, r1, max(1, host_cores() // max(1, local_world)))
+    t_gen = time.perf_counter() - t_gen
+
     import torch
     import torch.distributed as dist
 
     from paper_2005_11547_b200 import HashFamily, LshParams, _lib, lsh_batch, minhash_batch
-    from paper_2005_11547_b200 import workloads
 
-    rank, world, local = dist_env()
     # one rank per GPU; DSK_DIST_BACKEND=gloo (+ more ranks than GPUs) is only
     # for exercising the multi-rank code path on a one-GPU box, never timed
     backend = os.environ.get("DSK_DIST_BACKEND", "nccl")
@@ -240,20 +349,31 @@ def main():
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-    cfg = workloads.CONFIGS[args.workload]
-    k = args.k or (cfg.k[0] if cfg.k else 0)
-    n = args.sets or cfg.n
-    indptr, ids, w = workload_rows(cfg, rank, n)
+
+    def all_max(x):
+        t = torch.tensor([float(x)], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def all_sum(xs):
+        t = torch.tensor([float(x) for x in xs], dtype=torch.float64, device=red_dev)
+        if world > 1:
+            dist.all_reduce(t)
+        return [float(x) for x in t.tolist()]
+
+    n = r1 - r0
+    nnz = int(indptr[-1])
     fam = HashFamily(cfg.seed)
     lib = _lib.load()
     p_d = torch.from_numpy(indptr).to(dev)
     i_d = torch.from_numpy(ids.view(np.int64)).to(dev)
     w_d = torch.from_numpy(w).to(dev)
-    nnz = int(indptr[-1])
     onebit = cfg.onebit
+    lsh = cfg.kind == "lsh"
 
     def step():
-        if cfg.kind == "lsh":
+        if lsh:
             return lsh_batch(p_d, i_d, w_d, LshParams(cfg.L, cfg.K), fam, check=False)
         return minhash_batch(p_d, i_d, w_d, k, fam, bits=onebit, check=False)
 
@@ -264,26 +384,9 @@ def main():
     stats = res.stats.cpu().numpy().view(np.uint32).astype(np.int64)
     bad = int((status != 0).sum())
 
-    # K0: peak hash rates on this device (roofline denominators)
-    sink = torch.zeros(1, dtype=torch.int64, device=dev)
     ctx = fam.context(dev)
     stream = ctypes.c_void_p(torch.cuda.current_stream(dev).cuda_stream)
-
-    def hash_rate(mode, iters):
-        done = ctypes.c_int64()
-        lib.dsk_hash_peak(ctx, mode, 16, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(done),
-                          stream)
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        lib.dsk_hash_peak(ctx, mode, iters, ctypes.c_void_p(sink.data_ptr()), ctypes.byref(done),
-                          stream)
-        e1.record()
-        torch.cuda.synchronize()
-        return done.value / (e0.elapsed_time(e1) / 1000.0)
-
-    peak_hps = hash_rate(0, 256)          # full 22-lookup tabulation hash (reference's unit)
-    peak_hoisted_hps = hash_rate(1, 4096)  # one lookup + finalizer (hoisted lower bound on cost)
+    rates = unit_rates(lib, ctx, dev, stream)
 
     clocks = ClockSampler(local_dev)
     if world > 1:
@@ -302,131 +405,143 @@ def main():
     if world > 1:
         dist.barrier()
     clk = clocks.stop()
-    ms = start.elapsed_time(end) / args.steps
-    t = torch.tensor([ms], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_local = start.elapsed_time(end) / args.steps
+    ms_max = all_max(ms_local)
+    sec = ms_max / 1000.0
 
     # work units: areas A, candidate darts D, hits H at phi*
-    A, D, H = stats[:, 0].sum(), stats[:, 1].sum(), stats[:, 2].sum()
-    hashes = A + 2 * D + 2 * H + (cfg.L * cfg.K * n if cfg.kind == "lsh" else 0)
-    tot = torch.tensor([float(n), float(H), float(hashes)], dtype=torch.float64, device=red_dev)
-    if world > 1:
-        dist.all_reduce(tot)
-    sets_all, hits_all, hashes_all = (float(x) for x in tot.tolist())
-    sec = ms_max / 1000.0
+    A, D, H = (float(stats[:, c].sum()) for c in range(3))
+    LK = float(cfg.L * cfg.K * n) if lsh else 0.0
+    hashes = A + 2 * D + 2 * H + LK
+    sets_all, A_all, D_all, H_all, LK_all, hashes_all, bad_all = all_sum(
+        [n, A, D, H, LK, hashes, bad])
     value = sets_all / sec
-    out_bytes = n * (8 * k + 8 * ((k + 63) // 64) * onebit + 4 + 4 + 16) if cfg.kind != "lsh" \
-        else n * (8 * cfg.L + 24)
+    words = (k + 63) // 64
+    out_bytes = n * (8 * cfg.L + 24) if lsh else \
+        n * (8 * k + 8 * words * onebit + 4 + 4 + 16)
     hbm_bytes = 16 * nnz + 8 * (n + 1) + out_bytes
-    peak_hbm = 6543.1
+    peaks = {}
     try:
-        peak_hbm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))["hbm_gbs"])
-    except (OSError, KeyError, ValueError):
+        peaks = json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json")))
+    except (OSError, ValueError):
         pass
+    peak_hbm = float(peaks.get("hbm_gbs", 6543.1))
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
 
-    # e2e through the C ABI with host (pinned) buffers
-    e2e = None
+    # ------------------------------------------------------------ e2e legs
+    e2e = e2e_pageable = None
     if not args.no_e2e:
-        pin_p = torch.from_numpy(indptr).pin_memory()
-        pin_i = torch.from_numpy(ids.view(np.int64)).pin_memory()
-        pin_w = torch.from_numpy(w).pin_memory()
-        lsh = cfg.kind == "lsh"
-        o_v = torch.empty((n, cfg.L if lsh else k), dtype=torch.int64).pin_memory()
-        o_s = torch.empty(n, dtype=torch.int32).pin_memory()
-        words = (k + 63) // 64
-        o_b = torch.empty((n, words), dtype=torch.int64).pin_memory() if onebit else None
         api = "dsk_lsh_csr_host" if lsh else "dsk_minhash_csr_host"
-        P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
+        P = lambda a: ctypes.c_void_p(a.ctypes.data) if a is not None else None  # noqa: E731
 
-        def host_call():
+        def host_call(hp, hi, hw, ov, ob, os_):
             if lsh:
-                rc = lib.dsk_lsh_csr_host(ctx, P(pin_p), P(pin_i), P(pin_w), n, cfg.L, cfg.K, 0,
-                                          P(o_v), None, P(o_s), None, None)
+                rc = lib.dsk_lsh_csr_host(ctx, P(hp), P(hi), P(hw), n, cfg.L, cfg.K, 0,
+                                          P(ov), None, P(os_), None, None)
             else:
-                rc = lib.dsk_minhash_csr_host(ctx, P(pin_p), P(pin_i), P(pin_w), n, k, P(o_v),
-                                              P(o_b), P(o_s), None, None)
+                rc = lib.dsk_minhash_csr_host(ctx, P(hp), P(hi), P(hw), n, k, P(ov), P(ob),
+                                              P(os_), None, None)
             _lib.check(rc, api)
 
-        host_call()
-        if world > 1:
-            dist.barrier()
-        b0 = lib.dsk_h2d_bytes()
-        t0 = time.perf_counter()
-        for _ in range(args.steps):
-            host_call()
-        dt = (time.perf_counter() - t0) / args.steps
-        h2d_copied = (lib.dsk_h2d_bytes() - b0) // args.steps
-        tt = torch.tensor([dt], dtype=torch.float64, device=red_dev)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        dt = float(tt.item())
-        h2d = int(h2d_copied)  # as counted by the library (dsk_h2d_bytes)
-        d2h = o_v.numel() * 8 + o_s.numel() * 4 + (o_b.numel() * 8 if o_b is not None else 0)
-        e2e = {"value": sets_all / dt, "unit": "sketches/sec", "ms_per_step": dt * 1000.0,
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-               "api": f"{api} (C ABI, pinned host buffers)",
-               "input_bytes_per_step": int(indptr.nbytes + ids.nbytes + w.nbytes)}
-        assert (o_s.numpy() == 0).all()
+        def timed(bufs, label):
+            host_call(*bufs)
+            if world > 1:
+                dist.barrier()
+            b0 = lib.dsk_h2d_bytes()
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                host_call(*bufs)
+            dt = all_max((time.perf_counter() - t0) / args.steps)
+            h2d = (lib.dsk_h2d_bytes() - b0) // args.steps
+            ov, ob, os_ = bufs[3:]
+            d2h = ov.nbytes + os_.nbytes + (ob.nbytes if ob is not None else 0)
+            assert (os_ == 0).all(), "status != 0 on the host-buffer path"
+            return {"value": sets_all / dt, "unit": "sketches/sec", "ms_per_step": dt * 1000.0,
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "api": f"{api} (C ABI, {label})"}
 
-    cpu = None
+        cols = cfg.L if lsh else k
+        in_bytes = indptr.nbytes + ids.nbytes + w.nbytes
+        out_b = n * cols * 8 + n * 4 + (n * words * 8 if onebit else 0)
+        try:
+            import psutil
+            avail = psutil.virtual_memory().available
+        except ImportError:
+            avail = 1 << 40
+        if (in_bytes + out_b) * local_world < 0.3 * avail:
+            pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
+            bufs = (pin(indptr), pin(ids.view(np.int64)), pin(w),
+                    pin(np.empty((n, cols), np.int64)),
+                    pin(np.empty((n, words), np.int64)) if onebit else None,
+                    pin(np.empty(n, np.int32)))
+            e2e = timed(bufs, "pinned host buffers")
+            del bufs
+        pbufs = (indptr, ids, w, np.empty((n, cols), np.uint64),
+                 np.empty((n, words), np.uint64) if onebit else None, np.empty(n, np.int32))
+        e2e_pageable = timed(pbufs, "plain numpy arrays, the INTEGRATION.md binding")
+        if e2e is None:
+            e2e = e2e_pageable
+
+    cpu = port = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        cpu = cpu_baseline(cfg, k, indptr, ids, w, args.cpu_seconds, cfg.L, cfg.K)
+        port = cpu_port(cfg, k, indptr, ids, w, args.cpu_seconds)
+        cpu = cpu_reference(cfg, k, indptr, ids, w, args.cpu_seconds) or port
 
     if rank == 0:
-        traffic = None
-        issue = None
-        tkey = cfg.name if args.k is None else f"{cfg.name}_k{k}"
-        tpath = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "ncu_traffic.json")
-        entry = json.load(open(tpath)).get(tkey) if os.path.exists(tpath) else None
-        if entry and args.sets is None and "bytes_per_launch" in entry:
-            traffic = {"bytes_per_launch": entry["bytes_per_launch"],
-                       "algorithmic_bytes_per_launch": hbm_bytes,
-                       "source": entry["source"]}
-        if entry and "warp_instructions_per_set" in entry and clk.get("sm_mhz"):
-            # the binding resource: warp-instruction issue (4 per SM per clock)
-            ips = entry["warp_instructions_per_set"] * n / (ms_max / 1e3)
-            peak_ips = 4.0 * torch.cuda.get_device_properties(dev).multi_processor_count * \
-                float(clk["sm_mhz"]) * 1e6
+        entry = ncu_entry(cfg, k, args.k is not None)
+        issue = traffic = None
+        if entry and entry.get("dram_bytes_per_set"):
+            traffic = entry["dram_bytes_per_set"] * n
+        if entry and clk.get("sm_mhz"):
+            ips = entry["warp_instructions_per_set"] * n / sec
+            peak_ips = 4.0 * sms * float(clk["sm_mhz"]) * 1e6
             issue = {"bound": "issue", "achieved": ips / 1e9, "peak": peak_ips / 1e9,
-                     "unit": "G warp-inst/s", "frac": ips / peak_ips,
-                     "note": "ncu instruction count per set (profiles/ncu_traffic.json) x sets / "
-                             "kernel time, against 4 issues/clk/SM at the sampled SM clock"}
-        achieved = hashes_all / sec / 1e9
-        peak = peak_hps / 1e9
+                     "unit": "G warp-inst/s", "frac": ips / peak_ips, "traffic": traffic,
+                     "algorithmic_bytes": hbm_bytes,
+                     "source": entry.get("source"),
+                     "note": "the binding resource (SURVEY 8(d), north_star: INT/hash-ALU "
+                             "issue rate): ncu smsp__inst_executed per set of this workload's "
+                             "kernel x sets / kernel time, against 4 warp-instructions/clk/SM x "
+                             f"{sms} SMs at the sampled SM clock; traffic = that capture's "
+                             "dram__bytes_read+write per set x sets (bytes per launch)"}
+        useful_s = (A_all / rates[2] + D_all / rates[3] + H_all / rates[4] +
+                    (LK_all / rates[5] if lsh else 0.0)) / world
+        useful = {"bound": "alu-useful", "achieved": useful_s * 1000.0, "peak": ms_max,
+                  "unit": "ms/step", "frac": useful_s / sec,
+                  "unit_rates_G_per_s": {"ref_hash": rates[0] / 1e9, "hoisted_hash": rates[1] / 1e9,
+                                         "area": rates[2] / 1e9, "dart": rates[3] / 1e9,
+                                         "hit": rates[4] / 1e9, "mix64_step": rates[5] / 1e9},
+                  "note": "lower bound on the step time: A areas / area rate + D darts / dart "
+                          "rate + H hits / hit rate (+ L*K mix64 steps), each rate from the K0 "
+                          "unit microbenchmark (all SMs, no enumeration bookkeeping) in this "
+                          "run; frac = bound / measured kernel time"}
         line = {
             "metric": METRIC, "value": value, "unit": "sketches/sec", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "u64/f64", "data": "synthetic",
             "config": {"workload": cfg.name, "description": cfg.description,
-                       "sets_per_gpu": n, "nnz_per_gpu": nnz, "k": k,
+                       "sets": int(n_total), "sets_rank0": n, "nnz_rank0": nnz, "k": k or None,
                        "L": cfg.L or None, "K": cfg.K or None, "onebit": onebit,
                        "l2": f"inputs larger than L2 ({hbm_bytes / 1e9:.2f} GB per GPU per step)",
-                       "parallelism": f"row shards x{world}, no collective"},
-            "darts_per_sec": hits_all / sec,
+                       "parallelism": f"row shards x{world} (plan_shards_lengths), no collective",
+                       "host_generation_s": round(t_gen, 2)},
+            "darts_per_sec": H_all / sec,
             "hash_evals_per_sec": hashes_all / sec,
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": peak,
-                         "unit": "Ghash/s", "frac": achieved / peak, "traffic": traffic,
-                         "peak_hoisted": peak_hoisted_hps / 1e9,
-                         "frac_hoisted": achieved / (peak_hoisted_hps / 1e9),
-                         "note": "achieved = algorithmic hash evaluations A+2D+2H per set "
-                                 "(SURVEY 8d; each one 22-byte tabulation hash + splitmix64, "
-                                 "ref/randomness.py:121-131) per second of the sketch kernel; "
-                                 "peak = K0 mode 0, that full 22-lookup hash on all SMs, "
-                                 "measured this run; peak_hoisted = K0 mode 1 (1 lookup + "
-                                 "finalizer), the rate if every hash were fully hoisted"},
-            "roofline_hbm": {"bound": "hbm", "achieved": hbm_bytes / sec / 1e9 * 1.0,
-                             "peak": peak_hbm, "unit": "GB/s",
-                             "frac": hbm_bytes / sec / 1e9 / peak_hbm,
-                             "note": "16 B/nonzero + 8 B/set + outputs; peak = MEASURED_PEAKS.json"},
-            "roofline_issue": issue,
+            "roofline": issue,
+            "roofline_useful": useful,
+            "roofline_hbm": {"bound": "hbm", "achieved": hbm_bytes / sec / 1e9, "peak": peak_hbm,
+                             "unit": "GB/s", "frac": hbm_bytes / sec / 1e9 / peak_hbm,
+                             "note": "16 B/nonzero + 8 B/set + outputs (rank 0); peak = "
+                                     "MEASURED_PEAKS.json hbm_gbs"},
+            "ref_hash_rate_G_per_s": rates[0] / 1e9,
             "e2e": e2e,
+            "e2e_pageable": e2e_pageable,
             "cpu_baseline": cpu,
+            "cpu_port": port,
             "gpu_launches": launches,
             "clocks": clk,
-            "status_nonzero": bad,
+            "status_nonzero": int(bad_all),
             "phi_hist": np.bincount(stats[:, 3]).tolist(),
         }
         print(json.dumps(line), flush=True)

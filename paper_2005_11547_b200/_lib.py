@@ -18,8 +18,9 @@ REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB_PATH = os.environ.get("DSK_LIB_PATH") or os.path.join(PKG, "libdsk_b200.so")
 HEADER = os.path.join(REPO, "include", "dsk_b200.h")
-SOURCES = ["dsk_kernels.cu", "dsk_device.cuh", "dsk_engine.cuh", "dsk_lsh_kernel.cuh",
-           "dsk_lsh_host.cuh", "dsk_extra.cuh"]
+def _sources() -> list[str]:
+    """Every CUDA source of the library (dsk_kernels.cu includes the headers)."""
+    return sorted(f for f in os.listdir(CSRC) if f.endswith((".cu", ".cuh")))
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -44,7 +45,7 @@ def needs_build() -> bool:
     if not os.path.exists(LIB_PATH):
         return True
     mtime = os.path.getmtime(LIB_PATH)
-    deps = [os.path.join(CSRC, s) for s in SOURCES] + [HEADER]
+    deps = [os.path.join(CSRC, s) for s in _sources()] + [HEADER]
     return any(os.path.exists(d) and os.path.getmtime(d) > mtime for d in deps)
 
 

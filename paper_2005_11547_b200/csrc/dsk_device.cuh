@@ -216,7 +216,7 @@ struct ModU32 {
   int pow2;
 };
 
-__host__ inline ModU32 make_mod(uint32_t d) {
+__host__ __device__ inline ModU32 make_mod(uint32_t d) {
   ModU32 r;
   r.d = d;
   r.pow2 = (d & (d - 1)) == 0;

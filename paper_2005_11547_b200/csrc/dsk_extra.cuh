@@ -20,7 +20,7 @@ extern "C" int dsk_l1_csr(const int64_t *indptr, const double *weights, int64_t 
   if (!indptr || !weights || !out || n < 0) return set_err(DSK_EARG, "bad argument");
   if (n == 0) return DSK_OK;
   int grid = (int)((n + 7) / 8);
-  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid > c_sms() * 16) grid = c_sms() * 16;
   l1_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(indptr, weights, n, out); count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
@@ -89,14 +89,14 @@ extern "C" int dsk_dsk1_records(int32_t kind, int32_t k, uint64_t seed, const ui
   int64_t total = n * (20 + pbytes);
   if ((pbytes & 3) == 0 && ((uintptr_t)out & 3) == 0) {
     int64_t wgrid = (n + 7) / 8;  // 8 warps per block
-    int grid = (int)(wgrid < 148 * 64 ? wgrid : 148 * 64);
+    int grid = (int)(wgrid < c_sms() * 64 ? wgrid : c_sms() * 64);
     dsk1_words_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
         kind, (uint32_t)k, seed, payload, words, pbytes, n, reinterpret_cast<uint32_t *>(out)); count_launch();
     CUDA_TRY(cudaGetLastError());
     return DSK_OK;
   }
   int grid = (int)((total + 255) / 256);
-  if (grid > 148 * 32) grid = 148 * 32;
+  if (grid > c_sms() * 32) grid = c_sms() * 32;
   dsk1_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(kind, (uint32_t)k, seed, payload, words,
                                                       pbytes, n, out); count_launch();
   CUDA_TRY(cudaGetLastError());
@@ -140,7 +140,7 @@ extern "C" int dsk_exact_jaccard(const int64_t *a_ptr, const uint64_t *a_ids, co
     return set_err(DSK_EARG, "bad argument");
   if (npairs == 0) return DSK_OK;
   int grid = (int)((npairs + 255) / 256);
-  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid > c_sms() * 16) grid = c_sms() * 16;
   jaccard_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(a_ptr, a_ids, a_w, b_ptr, b_ids, b_w,
                                                          pa, pb, npairs, out); count_launch();
   CUDA_TRY(cudaGetLastError());

@@ -106,6 +106,20 @@ static int set_err(int code, const char *msg) {
 
 extern "C" const char *dsk_last_error(void) { return g_err.c_str(); }
 
+// SM count of the current device (grid caps of the context-free entry points)
+static int c_sms() {
+  static std::atomic<int> cache[64];
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  int v = cache[dev].load();
+  if (v <= 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0)
+      v = 148;
+    cache[dev].store(v);
+  }
+  return v;
+}
+
 extern "C" int64_t dsk_minhash_density(int64_t k) {
   if (k < 1) return -1;
   if (k == 1) return 1;
@@ -695,20 +709,35 @@ __global__ void pack_onebit_kernel(const uint64_t *v, int64_t n, int k, uint64_t
   }
 }
 
-// K0: hash-rate microbenchmarks, all SMs, four independent chains per
-// thread.  mode 0 (the roofline denominator): one full hash evaluation as
-// the reference defines it (ref/randomness.py:121-131) -- 22 table lookups,
-// one per key byte, from all 22 tables in shared memory, plus splitmix64;
-// the key bytes come from the previous outputs of the chain.  mode 1: the
-// cheapest hash the engine issues (one shared-memory word + splitmix64), an
-// upper bound for fully hoisted hashing.
+// K0: unit-cost microbenchmarks on all SMs, four independent chains per
+// thread, no enumeration bookkeeping.  Modes:
+//   0  the reference's hash unit (ref/randomness.py:121-131): 22 table
+//      lookups, one per key byte, from all 22 tables in shared memory, plus
+//      splitmix64 (key bytes taken from the chain's previous output);
+//   1  a fully hoisted hash: one shared-memory word + splitmix64;
+//   2  an area (ref/darthash.py:258-262): hoisted Poisson hash + the
+//      inverse-CDF count against the integer thresholds;
+//   3  a candidate dart (ref/darthash.py:279-284): hoisted U hash, the exact
+//      u53 -> double, rank = r0 + (r + u) * drho (three rounded fp64 ops) and
+//      the inclusive rank test;
+//   4  a hit (ref/darthash.py:293, ref/randomness.py:154-158,
+//      ref/sketching.py:93-99): fingerprint finalizer, the 8-lookup bucket
+//      hash, mod k, and a 128-bit shared-memory CAS minimum into k = 256 slots;
+//   5  one mix64 step (ref/randomness.py:160-166): 8 lookups + splitmix64.
+// Modes 2-5 price the work the reference's algorithm cannot avoid per unit;
+// bench.py sums A/rate2 + D/rate3 + H/rate4 (+ L*K/rate5) into the
+// useful-work lower bound on a step's time.
 __global__ void __launch_bounds__(512) hash_peak_kernel(const uint64_t *tab, int64_t iters,
                                                         int mode, uint64_t *sink) {
   __shared__ uint64_t ts[22 * 256];
+  __shared__ __align__(16) uint64_t slots[2 * 256];
   for (int i = threadIdx.x; i < 22 * 256; i += blockDim.x) ts[i] = tab[i];
+  for (int i = threadIdx.x; i < 256; i += blockDim.x) { slots[2 * i] = kEmptyRank; slots[2 * i + 1] = 0; }
   __syncthreads();
   uint64_t g = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
   uint64_t h[4] = {g * 4 + 1, g * 4 + 2, g * 4 + 3, g * 4 + 4};
+  double acc = 0.0;
+  uint32_t cnt = 0;
   if (mode == 0) {
     for (int64_t i = 0; i < iters; i++) {
 #pragma unroll
@@ -725,13 +754,71 @@ __global__ void __launch_bounds__(512) hash_peak_kernel(const uint64_t *tab, int
         h[c] = finalize(x);
       }
     }
-  } else {
+  } else if (mode == 1) {
     for (int64_t i = 0; i < iters; i++) {
 #pragma unroll
       for (int c = 0; c < 4; c++) h[c] = finalize(h[c] ^ ts[h[c] & 0xff]);
     }
+  } else if (mode == 2) {
+    for (int64_t i = 0; i < iters; i++) {
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        uint64_t X = finalize(h[c] ^ ts[(h[c] >> 3) & 0xff]) >> 11;
+        uint32_t k = (X >= 0xbc5ab1b16779cULL) + (X >= 0x178b56362cef38ULL) +
+                     (X >= 0x1d6e2bc3b82b06ULL) + (X >= 0x1f6472f2e6944bULL);
+        cnt += k;
+        h[c] = (h[c] + 0x9e3779b97f4a7c15ULL) ^ X;
+      }
+    }
+  } else if (mode == 3) {
+    const double L = 1.0 + 1e-9;
+    for (int64_t i = 0; i < iters; i++) {
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        uint64_t hu = finalize(h[c] ^ ts[(h[c] >> 5) & 0xff]);
+        double u = u53(hu);
+        uint32_t r = (uint32_t)h[c] & 7;
+        double rank = __dadd_rn(0.0, __dmul_rn(__dadd_rn((double)r, u), 0.125));
+        cnt += rank <= L;
+        h[c] = hu;
+      }
+    }
+  } else if (mode == 4) {
+    const ModU32 md = make_mod(256);
+    for (int64_t i = 0; i < iters; i++) {
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        uint64_t fp = finalize(h[c]);
+        uint64_t x = ts[20 * 256 + 5];
+#pragma unroll
+        for (int p = 0; p < 8; p++) x ^= ts[p * 256 + ((fp >> (8 * p)) & 0xff)];
+        uint64_t bh = finalize(x);
+        uint64_t *sl = slots + 2 * mod_u32(bh, md);
+        uint64_t rb = bh >> 12;  // a positive double's bit pattern stands in for the rank
+        uint64_t cr, cf;
+        ld128_shared(sl, cr, cf);
+        while (rb < cr || (rb == cr && fp < cf)) {
+          uint64_t orr, off;
+          cas128_shared(sl, cr, cf, rb, fp, orr, off);
+          if (orr == cr && off == cf) break;
+          cr = orr;
+          cf = off;
+        }
+        h[c] = fp + 0x9e3779b97f4a7c15ULL;
+      }
+    }
+  } else {
+    for (int64_t i = 0; i < iters; i++) {
+#pragma unroll
+      for (int c = 0; c < 4; c++) {
+        uint64_t x = ts[10 * 256 + (i & 0xff)];
+#pragma unroll
+        for (int p = 0; p < 8; p++) x ^= ts[p * 256 + ((h[c] >> (8 * p)) & 0xff)];
+        h[c] = finalize(x) ^ (h[c] * 3);
+      }
+    }
   }
-  uint64_t x = h[0] ^ h[1] ^ h[2] ^ h[3];
+  uint64_t x = h[0] ^ h[1] ^ h[2] ^ h[3] ^ cnt ^ (uint64_t)__double_as_longlong(acc);
   if (x == 0x9e3779b97f4a7c15ULL) sink[0] = x;  // practically never; keeps the work live
 }
 
@@ -1113,7 +1200,7 @@ extern "C" int dsk_pack_onebit(const uint64_t *values, int64_t n, int32_t k, uin
   if (n == 0) return DSK_OK;
   int64_t warps = n * ((k + 63) / 64);
   int grid = (int)((warps * 32 + 255) / 256);
-  if (grid > 148 * 16) grid = 148 * 16;
+  if (grid > c_sms() * 16) grid = c_sms() * 16;
   pack_onebit_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(values, n, k, out_bits); count_launch();
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;

@@ -20,17 +20,25 @@ import torch.distributed as dist
 
 
 def row_costs(indptr: np.ndarray, t: int) -> np.ndarray:
-    nnz = np.diff(np.asarray(indptr, dtype=np.int64))
-    return nnz.astype(np.float64) * 3.0 + 2.0 * float(t)
+    return length_costs(np.diff(np.asarray(indptr, dtype=np.int64)), t)
+
+
+def length_costs(lengths: np.ndarray, t: int) -> np.ndarray:
+    return np.asarray(lengths, dtype=np.float64) * 3.0 + 2.0 * float(t)
 
 
 def plan_shards(indptr, world: int, t: int = 1) -> np.ndarray:
     """Row boundaries (world+1,) of contiguous ranges with balanced cost."""
+    return plan_shards_lengths(np.diff(np.asarray(indptr, dtype=np.int64)), world, t)
+
+
+def plan_shards_lengths(lengths, world: int, t: int = 1) -> np.ndarray:
+    """plan_shards from the row lengths alone (workloads.lengths gives them
+    without generating the rows, so each rank can then generate only its own)."""
     if world < 1:
         raise ValueError("world must be >= 1")
-    indptr = np.asarray(indptr, dtype=np.int64)
-    n = indptr.size - 1
-    cost = row_costs(indptr, t)
+    cost = length_costs(lengths, t)
+    n = cost.size
     cum = np.concatenate([[0.0], np.cumsum(cost)])
     targets = cum[-1] * np.arange(1, world) / world
     cuts = np.searchsorted(cum, targets, side="left")

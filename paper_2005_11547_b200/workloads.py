@@ -73,12 +73,14 @@ def _distinct_rows(rng, d: int, lengths: np.ndarray) -> np.ndarray:
     ids = rng.integers(0, d, size=total, dtype=np.uint64)
     starts = np.zeros(lengths.size + 1, dtype=np.int64)
     np.cumsum(lengths, out=starts[1:])
-    row = np.repeat(np.arange(lengths.size, dtype=np.int64), lengths)
-    order = np.lexsort((ids, row))
-    sid = ids[order]
-    srow = row[order]
-    dup = (sid[1:] == sid[:-1]) & (srow[1:] == srow[:-1])
-    bad = np.unique(srow[1:][dup])
+    # rows holding a repeated id (ascending), found by sorting within rows
+    if lengths.size and (lengths == lengths[0]).all():
+        srt = np.sort(ids.reshape(lengths.size, int(lengths[0])), axis=1)
+        bad = np.flatnonzero((srt[:, 1:] == srt[:, :-1]).any(axis=1))
+    else:
+        row = np.repeat(np.arange(lengths.size, dtype=np.uint64), lengths)
+        key = np.sort(row * np.uint64(d) + ids)
+        bad = np.unique(key[1:][key[1:] == key[:-1]] // np.uint64(d)).astype(np.int64)
     for r in bad.tolist():  # rare: redraw the whole row without replacement
         a, b = starts[r], starts[r + 1]
         ids[a:b] = rng.choice(d, size=b - a, replace=False).astype(np.uint64)
@@ -103,12 +105,16 @@ def _weights(rng, kind: str, lengths: np.ndarray) -> np.ndarray:
     raise ValueError(kind)
 
 
+def _block_lengths(cfg: Workload, rng, rows: int) -> np.ndarray:
+    """The row lengths of one block: the first draws of the block's stream."""
+    if cfg.nnz == "zipf":
+        return np.minimum(rng.zipf(1.5, size=rows), 16384).astype(np.int64)
+    return np.full(rows, int(cfg.nnz), dtype=np.int64)
+
+
 def _gen_block(cfg: Workload, block: int, rows: int):
     rng = _block_rng(cfg.seed, block)
-    if cfg.nnz == "zipf":
-        lengths = np.minimum(rng.zipf(1.5, size=rows), 16384).astype(np.int64)
-    else:
-        lengths = np.full(rows, int(cfg.nnz), dtype=np.int64)
+    lengths = _block_lengths(cfg, rng, rows)
     if cfg.name == "cfg1":
         # d = 1e4 with nnz = 256: draw without replacement per set
         ids = np.concatenate([rng.choice(cfg.d, size=int(m), replace=False).astype(np.uint64)
@@ -119,29 +125,102 @@ def _gen_block(cfg: Workload, block: int, rows: int):
     return lengths, ids, w
 
 
-def generate(cfg_name: str, n: int | None = None, start: int = 0):
-    """CSR arrays for rows [start, start + n) of a configuration."""
+def _block_rows(cfg: Workload, b: int) -> int:
+    return min(BLOCK_ROWS, cfg.n - b * BLOCK_ROWS) if b * BLOCK_ROWS < cfg.n else BLOCK_ROWS
+
+
+def lengths(cfg_name: str, n: int | None = None, start: int = 0) -> np.ndarray:
+    """Row lengths (nnz) of rows [start, start + n) without generating the rows.
+
+    Only the first draws of each block's stream are made (the lengths come
+    first), so a shard plan over the full population (cfg5: 1e7 rows) costs
+    about a second on the host."""
     cfg = CONFIGS[cfg_name]
     if n is None:
         n = cfg.n - start
     end = start + n
+    if cfg.nnz != "zipf":
+        return np.full(n, int(cfg.nnz), dtype=np.int64)
+    out = []
+    for b in range(start // BLOCK_ROWS, (end + BLOCK_ROWS - 1) // BLOCK_ROWS):
+        rows = _block_rows(cfg, b)
+        ln = _block_lengths(cfg, _block_rng(cfg.seed, b), rows)
+        out.append(ln[max(start - b * BLOCK_ROWS, 0):min(end - b * BLOCK_ROWS, rows)])
+    return np.concatenate(out) if out else np.zeros(0, np.int64)
+
+
+# fork-inherited state of the block workers (one generate() call at a time)
+_POOL_JOB = None
+
+
+def _fill_block(task):
+    """Generate one block and copy its requested rows into the shared outputs."""
+    cfg, b, rows, lo, hi, e_out = task
+    ids_out, w_out = _POOL_JOB
+    ln, ids, w = _gen_block(cfg, b, rows)
+    offs = np.zeros(rows + 1, dtype=np.int64)
+    np.cumsum(ln, out=offs[1:])
+    m = int(offs[hi] - offs[lo])
+    ids_out[e_out:e_out + m] = ids[offs[lo]:offs[hi]]
+    w_out[e_out:e_out + m] = w[offs[lo]:offs[hi]]
+    return m
+
+
+def _shared_empty(count: int, dtype) -> np.ndarray:
+    import mmap
+    nbytes = max(1, count * np.dtype(dtype).itemsize)
+    return np.frombuffer(mmap.mmap(-1, nbytes), dtype=dtype, count=count)
+
+
+def default_workers() -> int:
+    import os
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:
+        return max(1, os.cpu_count() or 1)
+
+
+def generate(cfg_name: str, n: int | None = None, start: int = 0, workers: int | None = None):
+    """CSR arrays for rows [start, start + n) of a configuration.
+
+    Blocks of BLOCK_ROWS rows have independent streams, so they are generated
+    by a pool of forked host processes (`workers`, default: every core the
+    process may use) writing straight into shared output arrays; the bytes do
+    not depend on the worker count or on how the rows are split."""
+    global _POOL_JOB
+    cfg = CONFIGS[cfg_name]
+    if n is None:
+        n = cfg.n - start
+    end = start + n
+    lens = lengths(cfg_name, n, start)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    nnz = int(indptr[-1])
     b0, b1 = start // BLOCK_ROWS, (end + BLOCK_ROWS - 1) // BLOCK_ROWS
-    lens, idl, wl = [], [], []
+    tasks = []
     for b in range(b0, b1):
-        rows = min(BLOCK_ROWS, cfg.n - b * BLOCK_ROWS) if b * BLOCK_ROWS < cfg.n else BLOCK_ROWS
-        lengths, ids, w = _gen_block(cfg, b, rows)
-        lo = max(start - b * BLOCK_ROWS, 0)
-        hi = min(end - b * BLOCK_ROWS, rows)
-        offs = np.zeros(rows + 1, dtype=np.int64)
-        np.cumsum(lengths, out=offs[1:])
-        lens.append(lengths[lo:hi])
-        idl.append(ids[offs[lo]:offs[hi]])
-        wl.append(w[offs[lo]:offs[hi]])
-    lengths = np.concatenate(lens) if lens else np.zeros(0, np.int64)
-    indptr = np.zeros(lengths.size + 1, dtype=np.int64)
-    np.cumsum(lengths, out=indptr[1:])
-    ids = np.ascontiguousarray(np.concatenate(idl) if idl else np.zeros(0, np.uint64))
-    w = np.ascontiguousarray(np.concatenate(wl) if wl else np.zeros(0, np.float64))
+        rows = _block_rows(cfg, b)
+        lo, hi = max(start - b * BLOCK_ROWS, 0), min(end - b * BLOCK_ROWS, rows)
+        tasks.append((cfg, b, rows, lo, hi, int(indptr[b * BLOCK_ROWS + lo - start])))
+    workers = min(workers or default_workers(), len(tasks))
+    if workers > 1:
+        import multiprocessing as mp
+        ids, w = _shared_empty(nnz, np.uint64), _shared_empty(nnz, np.float64)
+        _POOL_JOB = (ids, w)
+        try:
+            with mp.get_context("fork").Pool(workers) as pool:
+                got = pool.map(_fill_block, tasks, chunksize=1)
+        finally:
+            _POOL_JOB = None
+        ids, w = np.array(ids, copy=True), np.array(w, copy=True)  # private, writable
+    else:
+        ids, w = np.empty(nnz, np.uint64), np.empty(nnz, np.float64)
+        _POOL_JOB = (ids, w)
+        try:
+            got = [_fill_block(t) for t in tasks]
+        finally:
+            _POOL_JOB = None
+    assert sum(got) == nnz
     return indptr, ids, w
 
 
