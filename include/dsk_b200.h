@@ -16,8 +16,15 @@
  *     only the uploaded hash-family constants and its scratch.
  *   - uint64 values are raw bit patterns (numpy uint64 / torch int64 views).
  *   - Per-set status: DSK_OK or one of the codes below.  Bit DSK_STATUS_TIE is
- *     OR-ed in when two darts of one slot had bit-identical fp64 ranks; the
- *     library then re-resolves the slot by full index tuple.
+ *     OR-ed in when two darts of one slot had bit-identical fp64 ranks: such a
+ *     slot holds the smaller fingerprint, while the reference orders equal
+ *     ranks by index tuple (ref/sketching.py:93-99).  C callers must handle a
+ *     tied row themselves (re-sketch it through the Python facade, whose
+ *     minhash_batch / lsh_batch / shard.minhash_host_multi re-resolve tied rows
+ *     by full index tuple on the GPU, or materialise its darts with
+ *     dsk_darts_csr at phi* and take the per-bucket minimum by index tuple).
+ *   - The C entry points take rows as given; duplicate element ids inside a
+ *     row (rejected by ref/core.py:42-43) are checked by the Python facade.
  *   - A context is read-only after creation: concurrent calls on different
  *     streams are safe.
  */
@@ -40,6 +47,7 @@ extern "C" {
 #define DSK_LIMIT 6    /* ValidationError rank limit <= 0 or infinite    ref/darthash.py:136-138 */
 #define DSK_SCRATCH 7  /* LSH hit buffer overflow (library limit, not a reference error) */
 #define DSK_TOOLARGE 8 /* reserved (no longer returned: large sets are enumerated in slices) */
+#define DSK_OVERFLOW 9 /* OverflowError: 1 + t*x_i is inf (math.floor(inf)) ref/darthash.py:154-156 */
 #define DSK_STATUS_TIE 0x100
 
 /* call-level error codes */

@@ -151,7 +151,7 @@ int or_weight_class(double l1) {
 }
 
 /* floor(math.log2(y)) as an int; returns INT32_MAX for inf/NaN (the
- * reference raises OverflowError there, mapped to OR_DEPTH). */
+ * reference raises OverflowError there, mapped to OR_OVERFLOW). */
 static int floor_log2(double y) {
   double l = log2(y);
   if (!isfinite(l)) return INT32_MAX;
@@ -216,6 +216,10 @@ int or_dart_batch(const uint64_t *tab, const double *cdf, int64_t t, const uint6
   for (int64_t i = 0; i < n; i++) { /* :154-156 */
     depth[i] = floor_log2(1.0 + tf * x[i]);
     if (depth[i] > max_depth) max_depth = depth[i];
+  }
+  if (max_depth == INT32_MAX) { /* :154-156: math.floor(math.log2(inf)) raises OverflowError */
+    free(depth);
+    return OR_OVERFLOW;
   }
   int rank_depth = floor_log2(1.0 + limit); /* :157 */
   if (max_depth > 255 || rank_depth > 255) { /* :159-160 */

@@ -16,6 +16,7 @@
 #define OR_EMPTY 1   /* ValidationError: empty set            ref/sketching.py:86-88 */
 #define OR_WEIGHT 2  /* ValidationError: weight not finite>0  ref/core.py:38-41 */
 #define OR_DEPTH 3   /* ValidationError: depth > 255          ref/darthash.py:158-160 */
+#define OR_OVERFLOW 9 /* OverflowError: 1 + t*x is inf          ref/darthash.py:154-156 */
 #define OR_AREAS 4   /* ValidationError: > 2^27 areas         ref/darthash.py:242-244 */
 #define OR_NOCONV 5  /* RuntimeError: 64 phi steps            ref/sketching.py:112 */
 #define OR_LIMIT 6   /* ValidationError: rank limit <=0 / inf ref/darthash.py:136-138 */

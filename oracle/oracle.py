@@ -24,7 +24,7 @@ _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 _lib = None
 
 STATUS_NAMES = {0: "ok", 1: "empty", 2: "weight", 3: "depth", 4: "areas",
-                5: "noconv", 6: "limit", 7: "badarg", 8: "nomem"}
+                5: "noconv", 6: "limit", 7: "badarg", 8: "nomem", 9: "overflow"}
 
 DART_DTYPE = np.dtype([
     ("element", "<u8"), ("nu", "<u2"), ("rho", "<u2"), ("w", "<u4"), ("r", "<u4"),

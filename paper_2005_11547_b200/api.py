@@ -32,6 +32,8 @@ from . import _lib, constants
 from .constants import ValidationError, minhash_density
 
 DSK_OK, DSK_EMPTY, DSK_WEIGHT, DSK_DEPTH, DSK_AREAS, DSK_NOCONV, DSK_LIMIT = range(7)
+DSK_OVERFLOW = 9
+DSK_DUP = 10  # facade-level: a row repeats an element id (ref/core.py:42-43)
 DSK_STATUS_TIE = 0x100
 
 _STATUS_ERRORS = {
@@ -43,6 +45,10 @@ _STATUS_ERRORS = {
     DSK_LIMIT: (ValidationError, "rank limit must be positive and finite"),
     7: (RuntimeError, "LSH hit buffer overflow (library limit)"),
     8: (RuntimeError, "set too large (reserved status)"),
+    # 1 + t*x_i overflows to inf: math.floor(math.log2(inf)) raises in the
+    # reference's depth computation (ref/darthash.py:154-156)
+    DSK_OVERFLOW: (OverflowError, "cannot convert float infinity to integer"),
+    DSK_DUP: (ValidationError, "duplicate element id"),
 }
 
 
@@ -413,14 +419,39 @@ def _csr_to_dev(indptr, ids, weights, dev):
     return p, i, w
 
 
-def raise_for_status(status: torch.Tensor, offset: int = 0) -> None:
-    """Raise the reference's exception for the first failing row (row order)."""
+def raise_for_status(status: torch.Tensor, offset: int = 0, dup_rows=None) -> None:
+    """Raise the reference's exception for the first failing row (row order).
+
+    `dup_rows` (sorted row indices whose ids repeat, from `_dup_rows`) fail
+    first on their row: the reference rejects them when the WeightedSet is
+    built (ref/core.py:42-43), before anything is sketched."""
     st = status.cpu().numpy() & 0xFF
     bad = np.nonzero(st)[0]
+    first_dup = int(dup_rows[0]) if dup_rows is not None and len(dup_rows) else None
+    if first_dup is not None and (not bad.size or first_dup <= int(bad[0])):
+        exc, msg = _STATUS_ERRORS[DSK_DUP]
+        raise exc(f"set {first_dup + offset}: {msg}")
     if bad.size:
         row = int(bad[0])
         exc, msg = _STATUS_ERRORS.get(int(st[row]), (RuntimeError, f"status {int(st[row])}"))
         raise exc(f"set {row + offset}: {msg}")
+
+
+def _dup_rows(p: torch.Tensor, i: torch.Tensor) -> np.ndarray:
+    """Rows of a device CSR batch that repeat an element id (ascending).
+
+    WeightedSet.from_arrays rejects them (ref/core.py:42-43); the batch
+    entry points take raw CSR, so the facade checks on the device: one
+    stable sort by id, one stable sort by row, adjacent equal (row, id)."""
+    n = p.numel() - 1
+    if i.numel() < 2 or n < 1:
+        return np.zeros(0, dtype=np.int64)
+    rows = torch.repeat_interleave(torch.arange(n, device=p.device), p[1:] - p[:-1])
+    o = torch.sort(i, stable=True).indices
+    o = o[torch.sort(rows[o], stable=True).indices]
+    si, sr = i[o], rows[o]
+    dup = (si[1:] == si[:-1]) & (sr[1:] == sr[:-1])
+    return torch.unique(sr[1:][dup]).cpu().numpy()
 
 
 def minhash_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, values: bool = True,
@@ -444,7 +475,7 @@ def minhash_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, values: b
             _ptr(out_b), _ptr(status), _ptr(phi), _ptr(st), _stream_ptr(dev)), "dsk_minhash_csr")
     res = MinhashBatch(out_v, out_b, status, phi, st)
     if check:
-        raise_for_status(status)
+        raise_for_status(status, dup_rows=_dup_rows(p, i))
         if bool(((status & DSK_STATUS_TIE) != 0).any()):
             _resolve_minhash_ties(res, p, i, w, k, hashes, dev)
     return res
@@ -470,7 +501,7 @@ def lsh_batch(indptr, ids, weights, params: LshParams, hashes: HashFamily, *,
             "dsk_lsh_csr")
     res = LshBatch(out_k, out_f, status, phi, st)
     if check:
-        raise_for_status(status)
+        raise_for_status(status, dup_rows=_dup_rows(p, i))
         if bool(((status & DSK_STATUS_TIE) != 0).any()):
             _resolve_lsh_ties(res, p, i, w, params, hashes, dev, normalize)
     return res
@@ -615,17 +646,18 @@ def _resolve_minhash_ties(res: MinhashBatch, p, i, w, k, hashes, dev) -> None:
     first = torch.ones_like(sb, dtype=torch.bool)
     first[1:] = sb[1:] != sb[:-1]
     sel = order[first]
+    # every bucket of a tied row is non-empty at phi*, so `sel` holds all k
+    # minima of those rows: rebuild them whole (values and/or packed bits)
+    fixed = torch.zeros((rows.size, k), dtype=torch.int64, device=dev)
+    fixed[owner[sel], bucket[sel]] = fp[sel]
     if res.values is not None:
-        res.values[tied[owner[sel]], bucket[sel]] = fp[sel]
+        res.values[tied] = fixed
     if res.bits is not None:
         words = res.bits.shape[1]
-        vals = res.values[tied] if res.values is not None else None
-        if vals is not None:
-            packed = torch.zeros((rows.size, words), dtype=torch.int64, device=dev)
-            _lib.check(_lib.load().dsk_pack_onebit(_ptr(vals.contiguous()), rows.size, k,
-                                                   _ptr(packed), _stream_ptr(dev)),
-                       "dsk_pack_onebit")
-            res.bits[tied] = packed
+        packed = torch.zeros((rows.size, words), dtype=torch.int64, device=dev)
+        _lib.check(_lib.load().dsk_pack_onebit(_ptr(fixed), rows.size, k, _ptr(packed),
+                                               _stream_ptr(dev)), "dsk_pack_onebit")
+        res.bits[tied] = packed
     res.status[tied] = res.status[tied] & 0xFF
 
 
@@ -757,7 +789,7 @@ def bottom_k_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, device=N
         phis[spill] = sub.phi
     res = BottomKBatch(cols, status, phis)
     if check:
-        raise_for_status(status)
+        raise_for_status(status, dup_rows=_dup_rows(p, i))
     return res
 
 
@@ -937,6 +969,17 @@ class DartBatch:
     def size(self) -> int:
         return int(self.element.size)
 
+    @classmethod
+    def empty(cls) -> "DartBatch":
+        """A batch of no darts with the reference's column dtypes (ref/darthash.py:59-64)."""
+        return cls(np.empty(0, np.uint64), np.empty(0, np.uint16), np.empty(0, np.uint16),
+                   np.empty(0, np.uint32), np.empty(0, np.uint32), np.empty(0, np.uint16),
+                   np.empty(0, np.float64), np.empty(0, np.float64), np.empty(0, np.uint64))
+
+    def take(self, indices) -> "DartBatch":
+        """The rows at `indices`, every column (ref/darthash.py:66-67)."""
+        return DartBatch(*(getattr(self, name)[indices] for name in self.__slots__))
+
     def index_sort_keys(self):
         return (self.j, self.r, self.w, self.rho, self.nu, self.element)
 
@@ -1042,7 +1085,7 @@ def icws_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, device=None,
                    "dsk_icws_csr")
     res = IcwsBatch(el, tk, status)
     if check:
-        raise_for_status(status)
+        raise_for_status(status, dup_rows=_dup_rows(p, i))
     return res
 
 

@@ -124,7 +124,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) bottomk_kernel(BottomKArgs a) 
         const double L = __ddiv_rn((double)phi, l1);
         if (!(L > 0.0) || isinf(L)) { status = DSK_LIMIT; break; }
         const int RD = floor_log2_host(__dadd_rn(1.0, L), T.l2thr);
-        if (maxd > 255 || RD > 255) { status = DSK_DEPTH; break; }
+        if (depth_status(maxd, RD)) { status = depth_status(maxd, RD); break; }
         PassParams P;
         P.gtab = a.tabs.tab;
         P.inv_t = a.inv_t;

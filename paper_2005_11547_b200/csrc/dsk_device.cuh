@@ -40,13 +40,26 @@ __device__ __forceinline__ double u53(uint64_t h) {
 
 // floor(math.log2(y)) for y >= 1 using the host-probed threshold table:
 // thr[n] = smallest double below 2^n whose host log2 floors to n (else 2^n).
-// Returns 1024 for inf (the reference raises there; mapped to DSK_DEPTH).
+// Returns kDepthHuge for finite y >= 2^256 (the reference's depth > 255
+// ValidationError) and kDepthInf for y = inf (math.floor(inf) raises
+// OverflowError there, ref/darthash.py:154-156); see depth_status().
+constexpr int kDepthHuge = 1024, kDepthInf = 2048;
+
 __device__ __forceinline__ int floor_log2_host(double y, const double *thr) {
   if (!(y >= 1.0)) return 0;  // only reachable for invalid weights (status DSK_WEIGHT)
   uint64_t b = (uint64_t)__double_as_longlong(y);
   int e = (int)((b >> 52) & 0x7ff) - 1023;
-  if (e >= 256) return 1024;
+  if (e >= 256) return e == 1024 ? kDepthInf : kDepthHuge;
   return e + (y >= thr[e + 1] ? 1 : 0);
+}
+
+// Status of a step's depths (ref/darthash.py:154-160): an element depth of
+// inf raises OverflowError while the depths are computed, before the
+// range check; then any depth or rank depth > 255 is a ValidationError.
+__device__ __forceinline__ int depth_status(int maxd, int rank_depth) {
+  if (maxd >= kDepthInf) return 9;  // DSK_OVERFLOW
+  if (maxd > 255 || rank_depth > 255) return 3;  // DSK_DEPTH
+  return 0;
 }
 
 // _largest_passing, ref/darthash.py:80-95, for the rank side:

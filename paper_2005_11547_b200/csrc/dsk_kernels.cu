@@ -454,7 +454,7 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
         double L = __ddiv_rn((double)phi, l1);
         if (!(L > 0.0) || isinf(L)) { status = DSK_LIMIT; break; }
         int RD = floor_log2_host(__dadd_rn(1.0, L), T.l2thr);
-        if (maxd > 255 || RD > 255) { status = DSK_DEPTH; break; }
+        if (depth_status(maxd, RD)) { status = depth_status(maxd, RD); break; }
         PassParams P;
         P.gtab = a.tabs.tab;
         P.inv_t = a.inv_t;
@@ -600,7 +600,7 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
     }
     maxd = __reduce_max_sync(DSK_FULL, (unsigned)maxd);
     int RD = status == 0 ? floor_log2_host(__dadd_rn(1.0, L), T.l2thr) : 0;
-    if (status == 0 && (maxd > 255 || RD > 255)) status = DSK_DEPTH;  // :158-160
+    if (status == 0) status = depth_status(maxd, RD);  // :154-160
     if (lane == 0) cursors[warp] = 0;
     __syncwarp();
     if (status == 0) {

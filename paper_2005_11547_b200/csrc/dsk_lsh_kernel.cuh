@@ -195,7 +195,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         double Lim = __ddiv_rn((double)phi, l1);
         if (!(Lim > 0.0) || isinf(Lim)) { status = DSK_LIMIT; break; }
         int RD = floor_log2_host(__dadd_rn(1.0, Lim), T.l2thr);
-        if (maxd > 255 || RD > 255) { status = DSK_DEPTH; break; }
+        if (depth_status(maxd, RD)) { status = depth_status(maxd, RD); break; }
         PassParams P;
         P.gtab = a.tabs.tab;
         P.inv_t = a.inv_t;
