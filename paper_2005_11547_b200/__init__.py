@@ -7,7 +7,7 @@ The public names mirror the reference package `dartsketch`
 DESIGN.md for the boundary and INTEGRATION.md for the ctypes binding.
 """
 
-from .constants import ValidationError, minhash_density
+from .constants import ValidationError, derive_seed, minhash_density
 from . import io, shard, workloads
 from .api import (
     DSK_STATUS_TIE,
@@ -48,6 +48,7 @@ from .api import (
     one_bit,
     raise_for_status,
     weight_class,
+    exact_jaccard,
 )
 
 __all__ = [
@@ -58,7 +59,7 @@ __all__ = [
     "BottomKBatch", "BottomKFingerprints", "BottomKSketch", "bottom_k", "bottom_k_batch",
     "dump_sketch", "dump_sketches", "iter_sketches", "l1_batch", "load_sketch",
     "IcwsBatch", "IcwsHashValue", "IcwsSketcher", "icws_batch", "icws_estimate_jaccard",
-    "icws_fingerprints", "icws_minhash",
+    "icws_fingerprints", "icws_minhash", "exact_jaccard", "derive_seed",
 ]
 
 from .lsh_index import LshIndex, probe_classes  # noqa: E402

@@ -956,6 +956,29 @@ def lsh_key(x: WeightedSet, params: LshParams, hashes: HashFamily):
     return [tuple(int(v) for v in row) for row in fps]
 
 
+def exact_jaccard(x: WeightedSet, y: WeightedSet, *, device=None) -> float:
+    """Weighted Jaccard similarity sum(min) / sum(max) (ref/core.py:103-120),
+    computed by the dsk_exact_jaccard kernel: both rows merged in ascending id
+    order with sequential fp64 sums, as the reference's loop over
+    sorted(union) does.  Raises ValidationError for two empty sets."""
+    if x.is_empty() and y.is_empty():
+        raise ValidationError("Jaccard similarity is undefined for two empty sets")
+    dev = _device(device)
+    ox, oy = np.argsort(x.ids, kind="stable"), np.argsort(y.ids, kind="stable")
+    indptr = np.array([0, x.ids.size, x.ids.size + y.ids.size], dtype=np.int64)
+    ids = np.concatenate([x.ids[ox], y.ids[oy]]).astype(np.uint64)
+    ws = np.concatenate([x.weights[ox], y.weights[oy]]).astype(np.float64)
+    p, i, w = _csr_to_dev(indptr, ids, ws, dev)
+    pa = torch.zeros(1, dtype=torch.int64, device=dev)
+    pb = torch.ones(1, dtype=torch.int64, device=dev)
+    out = torch.empty(1, dtype=torch.float64, device=dev)
+    with torch.cuda.device(dev):
+        _lib.check(_lib.load().dsk_exact_jaccard(_ptr(p), _ptr(i), _ptr(w), _ptr(p), _ptr(i),
+                                                 _ptr(w), _ptr(pa), _ptr(pb), 1, _ptr(out),
+                                                 _stream_ptr(dev)), "dsk_exact_jaccard")
+    return float(out.item())
+
+
 class DartBatch:
     """Column-oriented darts (ref/darthash.py:39-77)."""
 
@@ -1039,7 +1062,7 @@ __all__ = [
     "MinhashBatch", "LshBatch", "ValidationError", "raise_for_status", "as_u64",
     "DSK_STATUS_TIE", "l1_batch", "bottom_k_batch", "BottomKBatch", "BottomKSketch",
     "BottomKFingerprints", "bottom_k", "dump_sketches", "dump_sketch", "iter_sketches",
-    "load_sketch",
+    "load_sketch", "exact_jaccard",
 ]
 _ = dataclasses
 

@@ -30,6 +30,13 @@ class ValidationError(ValueError):
     """Raised when input data violates a construction contract (ref/core.py:19-20)."""
 
 
+def derive_seed(base: int, *indices: int) -> int:
+    """A 64-bit seed derived from a base seed and indices (ref/randomness.py:89-92):
+    the first word of SeedSequence(base, spawn_key=indices)."""
+    seq = np.random.SeedSequence(base, spawn_key=tuple(indices))
+    return int(seq.generate_state(1, np.uint64)[0])
+
+
 def hash_tables(seed: int) -> np.ndarray:
     seed = int(seed)
     if not 0 <= seed <= 2**64 - 1:

@@ -143,4 +143,33 @@ def minhash_host_multi(indptr, ids, weights, k: int, hashes, *, devices=None, bi
         _lib.check(rc, "dsk_minhash_csr_host")
     if check:
         raise_for_status(torch.from_numpy(status))
+        repair_tied_rows(indptr, ids, weights, k, hashes, values, packed, status,
+                         device=devices[0])
     return values, packed, status
+
+
+def repair_tied_rows(indptr, ids, weights, k: int, hashes, values, packed, status, *,
+                     device=0) -> int:
+    """Re-resolve host-path rows flagged DSK_STATUS_TIE by full index tuple.
+
+    The C entry points order bit-identical ranks by fingerprint; the
+    reference orders them by index tuple (ref/sketching.py:93-99).  Flagged
+    rows are re-sketched through minhash_batch, whose tie path materialises
+    their darts at phi* on the GPU and takes each bucket's minimum by
+    (rank, element, nu, rho, w, r, j); the repaired rows overwrite `values`,
+    `packed` and `status` in place.  Returns the number of rows repaired."""
+    from .api import DSK_STATUS_TIE, as_u64, minhash_batch
+    from .workloads import subset
+    rows = np.nonzero((status & DSK_STATUS_TIE) != 0)[0]
+    if rows.size == 0:
+        return 0
+    sp, si, sw = subset(indptr, ids, weights, rows)
+    res = minhash_batch(sp, si, sw, k, hashes, values=values is not None,
+                        bits=packed is not None, stats=False,
+                        device=torch.device("cuda", int(device)))
+    if values is not None:
+        values[rows] = as_u64(res.values)
+    if packed is not None:
+        packed[rows] = as_u64(res.bits)
+    status[rows] = res.status.cpu().numpy()
+    return int(rows.size)

@@ -56,10 +56,7 @@ CONFIGS = {
 }
 
 
-def derive_seed(base: int, *indices: int) -> int:
-    """ref/randomness.py:89-92."""
-    seq = np.random.SeedSequence(base, spawn_key=tuple(indices))
-    return int(seq.generate_state(1, np.uint64)[0])
+from .constants import derive_seed  # noqa: E402  (ref/randomness.py:89-92)
 
 
 def _block_rng(seed: int, block: int) -> np.random.Generator:

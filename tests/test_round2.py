@@ -1,0 +1,258 @@
+"""Fidelity checks added in round 2: OverflowError depths, duplicate ids,
+the set-file reader and the GPU `sketch` command, the reference names the
+facade mirrors (DartBatch.empty/take, exact_jaccard, derive_seed), tie repair
+on the host-buffer path, and the shard plan from row lengths."""
+
+from __future__ import annotations
+
+import math
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import REPO, golden
+
+from oracle.oracle import Oracle
+from paper_2005_11547_b200 import (DartBatch, ValidationError, derive_seed, shard, workloads)
+from paper_2005_11547_b200 import io as dio
+
+
+# ----------------------------------------------------------------- CPU side
+
+def test_derive_seed_known_answer():
+    # the reference's derive_seed(1, 2, 3) (ref/randomness.py:89-92), run in the build container
+    assert derive_seed(1, 2, 3) == 10928566898365450891
+    assert workloads.derive_seed is derive_seed
+
+
+def test_dartbatch_empty_and_take():
+    e = DartBatch.empty()
+    assert e.size == 0
+    assert [getattr(e, n).dtype for n in DartBatch.__slots__] == [
+        np.uint64, np.uint16, np.uint16, np.uint32, np.uint32, np.uint16, np.float64, np.float64,
+        np.uint64]
+    cols = [np.arange(5, dtype=getattr(e, n).dtype) + i for i, n in enumerate(DartBatch.__slots__)]
+    b = DartBatch(*cols).take(np.array([4, 1]))
+    assert b.size == 2
+    for i, n in enumerate(DartBatch.__slots__):
+        assert getattr(b, n).tolist() == [4 + i, 1 + i]
+
+
+def test_oracle_overflow_statuses():
+    """The C oracle maps 1 + t*x = inf to OverflowError (status 9), a finite
+    depth > 255 to ValidationError (3) and l1 = inf to the limit error (6),
+    as the reference does (tests/golden/overflow.npz, made by the reference)."""
+    g = golden("overflow.npz")
+    orc = Oracle(int(g["seed"]))
+    for k in (1, 64):
+        _, status, _, _ = orc.minhash_csr(g["indptr"], g["ids"], g["w"], k)
+        assert status.tolist() == g[f"status_k{k}"].tolist()
+    _, _, status, _, _ = orc.lsh_csr(g["indptr"], g["ids"], g["w"], 4, 2)
+    assert status.tolist() == g["status_lsh"].tolist()
+
+
+def _cli_golden_text():
+    g = golden("cli_sketch.npz")
+    return g, g["text"].tobytes().decode()
+
+
+def test_read_csr_matches_the_reference_text(tmp_path):
+    """read_csr drops blank lines and zero weights; writing the CSR back gives
+    the reference's format_set text of every kept pair."""
+    g, text = _cli_golden_text()
+    path = tmp_path / "sets.txt"
+    path.write_text(text)
+    indptr, ids, w = dio.read_csr(path)
+    expect = []
+    for line in text.split("\n"):
+        if not line.strip():
+            continue
+        toks = [t for t in line.split() if float(t.partition(":")[2]) != 0.0]
+        expect.append(" ".join(toks))
+    assert indptr.size - 1 == len(expect)
+    out = tmp_path / "back.txt"
+    dio.write_csr(out, indptr, ids, w)
+    assert out.read_text() == "\n".join(expect) + "\n"
+    sets = dio.read_sets(path)
+    assert [x.l0 for x in sets] == np.diff(indptr).tolist()
+    assert all(x.l1 == float(np.sum(x.weights)) for x in sets)
+
+
+@pytest.mark.parametrize("name", ["neg_then_malformed", "malformed", "dup", "range", "nonfinite",
+                                  "inf"])
+def test_cli_parse_errors_match_the_reference(tmp_path, name):
+    """Bad set files: same exit code and stderr as `dartsketch sketch`
+    (ref/cli.py:107-131, ref/core.py:69-100), before any GPU work."""
+    g = golden("cli_sketch.npz")
+    path = tmp_path / f"{name}.txt"
+    path.write_bytes(g[f"badtext_{name}"].tobytes())
+    proc = subprocess.run([sys.executable, "-m", "paper_2005_11547_b200.cli", "sketch",
+                           "--input", str(path), "--out", str(tmp_path / "o.dsk")],
+                          cwd=REPO, capture_output=True, text=True, timeout=300)
+    assert proc.returncode == int(g[f"badrc_{name}"])
+    assert proc.stderr.replace(str(path), "<path>") == str(g[f"baderr_{name}"])
+
+
+def test_plan_shards_lengths_matches_plan_shards():
+    lens = workloads.lengths("cfg5", 50000, start=1234)
+    indptr = np.zeros(lens.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    for world in (1, 2, 3, 8):
+        a = shard.plan_shards(indptr, world, 750)
+        b = shard.plan_shards_lengths(lens, world, 750)
+        assert np.array_equal(a, b)
+        assert a[0] == 0 and a[-1] == lens.size and (np.diff(a) >= 0).all()
+
+
+def test_generate_is_independent_of_workers_and_split():
+    """Rows come out identical whatever the worker count and row range."""
+    a = workloads.generate("cfg5", n=70000, start=60000, workers=1)
+    b = workloads.generate("cfg5", n=70000, start=60000, workers=4)
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    p, i, w = workloads.generate("cfg5", n=30000, start=90000, workers=2)
+    lo, hi = a[0][30000], a[0][60000]
+    assert np.array_equal(p, a[0][30000:60001] - lo)
+    assert np.array_equal(i, a[1][lo:hi]) and np.array_equal(w, a[2][lo:hi])
+    assert np.array_equal(np.diff(a[0]), workloads.lengths("cfg5", 70000, start=60000))
+
+
+# ----------------------------------------------------------------- GPU side
+
+@pytest.mark.gpu
+def test_overflow_statuses_and_exceptions():
+    from paper_2005_11547_b200 import HashFamily, LshParams, lsh_batch, minhash_batch
+    g = golden("overflow.npz")
+    f = HashFamily(int(g["seed"]))
+    for k in (1, 64):
+        res = minhash_batch(g["indptr"], g["ids"], g["w"], k, f, check=False)
+        assert (res.status.cpu().numpy() & 0xFF).tolist() == g[f"status_k{k}"].tolist()
+    res = lsh_batch(g["indptr"], g["ids"], g["w"], LshParams(4, 2), f, check=False)
+    assert (res.status.cpu().numpy() & 0xFF).tolist() == g["status_lsh"].tolist()
+    # the first row raises what the reference raises: OverflowError at k = 64
+    with pytest.raises(OverflowError):
+        minhash_batch(g["indptr"][:2], g["ids"][:1], g["w"][:1], 64, f)
+    with pytest.raises(ValidationError, match="norm range"):
+        minhash_batch(g["indptr"][:2], g["ids"][:1], g["w"][:1], 1, f)
+
+
+@pytest.mark.gpu
+def test_duplicate_ids_rejected_in_row_order():
+    from paper_2005_11547_b200 import HashFamily, LshParams, lsh_batch, minhash_batch
+    indptr = np.array([0, 2, 4, 5, 7], dtype=np.int64)
+    ids = np.array([1, 2, 3, 4, 0, 9, 9], dtype=np.uint64)
+    w = np.array([0.5, 0.25, 1.0, 2.0, 0.0, 1.0, 2.0])  # row 2: bad weight; row 3: dup
+    f = HashFamily(1)
+    with pytest.raises(ValidationError, match="set 2: weights must be finite"):
+        minhash_batch(indptr, ids, w, 8, f)
+    w[4] = 1.0
+    with pytest.raises(ValidationError, match="set 3: duplicate element id"):
+        minhash_batch(indptr, ids, w, 8, f)
+    with pytest.raises(ValidationError, match="set 3: duplicate element id"):
+        lsh_batch(indptr, ids, w, LshParams(4, 2), f)
+    res = minhash_batch(indptr, ids, w, 8, f, check=False)  # unchecked: rows run as given
+    assert res.values.shape == (4, 8)
+
+
+@pytest.mark.gpu
+def test_exact_jaccard_matches_the_reference_loop():
+    from paper_2005_11547_b200 import WeightedSet, exact_jaccard
+    rng = np.random.default_rng(5)
+    for _ in range(20):
+        a = rng.choice(200, size=int(rng.integers(0, 60)), replace=False).astype(np.uint64)
+        b = np.concatenate([a[:len(a) // 2],
+                            rng.choice(np.arange(200, 400), size=int(rng.integers(1, 40)),
+                                       replace=False)]).astype(np.uint64)
+        x = WeightedSet.from_arrays(a, rng.random(a.size) + 1e-3)
+        y = WeightedSet.from_arrays(b, rng.random(b.size) + 1e-3)
+        xm = dict(zip(x.ids.tolist(), x.weights.tolist()))
+        ym = dict(zip(y.ids.tolist(), y.weights.tolist()))
+        mn = mx = 0.0
+        for e in sorted(xm.keys() | ym.keys()):  # ref/core.py:111-119
+            mn += min(xm.get(e, 0.0), ym.get(e, 0.0))
+            mx += max(xm.get(e, 0.0), ym.get(e, 0.0))
+        assert exact_jaccard(x, y) == mn / mx
+        assert exact_jaccard(y, x) == mn / mx
+    e = WeightedSet.from_arrays(np.zeros(0, np.uint64), np.zeros(0))
+    with pytest.raises(ValidationError):
+        exact_jaccard(e, e)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("algo", ["dartminhash", "icws", "icws-fast", "bottomk"])
+@pytest.mark.parametrize("one_bit", [False, True])
+def test_cli_sketch_byte_identical(tmp_path, algo, one_bit):
+    """`cli sketch` writes the same DSK1 bytes (and errors) as the reference's
+    `dartsketch sketch` on the same set file (tests/golden/cli_sketch.npz)."""
+    g, text = _cli_golden_text()
+    src = tmp_path / "sets.txt"
+    src.write_text(text)
+    dst = tmp_path / "out.dsk"
+    tag = f"{algo.replace('-', '_')}_{'onebit' if one_bit else 'full'}"
+    proc = subprocess.run([sys.executable, "-m", "paper_2005_11547_b200.cli", "sketch",
+                           "--input", str(src), "--out", str(dst), "--algo", algo, "--k", "64",
+                           "--seed", "7"] + (["--one-bit"] if one_bit else []),
+                          cwd=REPO, capture_output=True, text=True, timeout=600)
+    assert proc.returncode == int(g[f"rc_{tag}"]), proc.stderr
+    assert proc.stderr == str(g[f"err_{tag}"])
+    if proc.returncode == 0:
+        assert dst.read_bytes() == g[f"out_{tag}"].tobytes()
+
+
+@pytest.mark.gpu
+def test_cli_empty_set_error(tmp_path):
+    g = golden("cli_sketch.npz")
+    path = tmp_path / "e.txt"
+    path.write_bytes(g["badtext_empty_set"].tobytes())
+    proc = subprocess.run([sys.executable, "-m", "paper_2005_11547_b200.cli", "sketch",
+                           "--input", str(path), "--out", str(tmp_path / "o.dsk")],
+                          cwd=REPO, capture_output=True, text=True, timeout=300)
+    assert proc.returncode == int(g["badrc_empty_set"])
+    assert proc.stderr == str(g["baderr_empty_set"])
+
+
+@pytest.mark.gpu
+def test_host_multi_repairs_tied_rows():
+    """minhash_host_multi re-resolves DSK_STATUS_TIE rows by index tuple (the
+    C entry points leave them fingerprint-ordered): force the repair on
+    corrupted rows and get the reference's values and bits back."""
+    from paper_2005_11547_b200 import DSK_STATUS_TIE, HashFamily, as_u64, minhash_batch
+    from paper_2005_11547_b200.shard import minhash_host_multi, repair_tied_rows
+    indptr, ids, w = workloads.generate("cfg1", n=50)
+    f = HashFamily(0)
+    vals, bits, status = minhash_host_multi(indptr, ids, w, 64, f, devices=[0], bits=True)
+    good = minhash_batch(indptr, ids, w, 64, f, bits=True)
+    assert np.array_equal(vals, as_u64(good.values)) and np.array_equal(bits, as_u64(good.bits))
+    rows = [4, 20, 41]
+    vals[rows] = 7
+    bits[rows] = 0
+    status[rows] |= DSK_STATUS_TIE
+    assert repair_tied_rows(indptr, ids, w, 64, f, vals, bits, status) == 3
+    assert np.array_equal(vals, as_u64(good.values)) and np.array_equal(bits, as_u64(good.bits))
+    assert (status == 0).all()
+
+
+@pytest.mark.gpu
+def test_bits_only_tie_resolution():
+    """With values=False the tie path rebuilds the packed words of tied rows
+    from the re-resolved minima."""
+    import torch
+
+    from paper_2005_11547_b200 import DSK_STATUS_TIE, HashFamily, api, as_u64, minhash_batch
+    indptr, ids, w = workloads.generate("cfg3", n=30)
+    f = HashFamily(2)
+    good = as_u64(minhash_batch(indptr, ids, w, 256, f, bits=True).bits).copy()
+    res = minhash_batch(indptr, ids, w, 256, f, values=False, bits=True)
+    rows = torch.tensor([2, 11], device=res.bits.device)
+    res.bits[rows] = 0
+    res.status[rows] |= DSK_STATUS_TIE
+    dev = res.bits.device
+    p = torch.from_numpy(indptr).to(dev)
+    i = torch.from_numpy(ids.view(np.int64)).to(dev)
+    ww = torch.from_numpy(w).to(dev)
+    api._resolve_minhash_ties(res, p, i, ww, 256, f, dev)
+    assert np.array_equal(as_u64(res.bits), good)
+    assert (res.status.cpu().numpy() == 0).all()
