@@ -48,6 +48,7 @@ extern "C" {
 #define DSK_SCRATCH 7  /* LSH hit buffer overflow (library limit, not a reference error) */
 #define DSK_TOOLARGE 8 /* reserved (no longer returned: large sets are enumerated in slices) */
 #define DSK_OVERFLOW 9 /* OverflowError: 1 + t*x_i is inf (math.floor(inf)) ref/darthash.py:154-156 */
+#define DSK_RETRY 11   /* internal: an LSH row whose phi0 = 2 first band failed; never returned */
 #define DSK_STATUS_TIE 0x100
 
 /* call-level error codes */

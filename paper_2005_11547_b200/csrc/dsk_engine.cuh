@@ -98,7 +98,7 @@ struct SmemTables {
   uint64_t cfold;         // T12[0]^T13[0]^T16[0]^T17[0] (w, r < 2^16)
   uint64_t nfold;         // T11[0]^T15[0]               (w, r < 2^8)
   uint64_t bconst;        // bucket hash constant: T8..T19 at 0, stream 5
-  uint64_t pad;
+  uint64_t dfold;         // T9[0]^T10[0]^T11[0]^cfold: the constant bytes of a rho = 0, w = 0 area
 };
 
 struct WarpQueues {
@@ -145,25 +145,35 @@ struct DartRow {
   uint64_t fp;
 };
 
-// The first four integer thresholds ceil(cdf[m] * 2^53) of the reference's
-// POISSON1_CDF (ref/randomness.py:66-85) as immediates: dsk_ctx_create checks
-// that the CDF it is given reproduces them (and rejects any other CDF).
+// The first six integer thresholds ceil(cdf[m] * 2^53) of the reference's
+// POISSON1_CDF (ref/randomness.py:66-85) as immediates, pre-shifted to the
+// 64-bit hash domain: X = h >> 11 >= t  <=>  h >= t << 11 (t < 2^53), so the
+// count needs no shift.  dsk_ctx_create checks that the CDF it is given
+// reproduces them (and rejects any other CDF).
 constexpr uint64_t kPt0 = 0xbc5ab1b16779cULL, kPt1 = 0x178b56362cef38ULL,
-                   kPt2 = 0x1d6e2bc3b82b06ULL, kPt3 = 0x1f6472f2e6944bULL;
+                   kPt2 = 0x1d6e2bc3b82b06ULL, kPt3 = 0x1f6472f2e6944bULL,
+                   kPt4 = 0x1fe204beb22e9cULL, kPt5 = 0x1ffb21e77480acULL;
 
-// Poisson(1) count: #{m : X >= thr[m]} (inverse CDF, ref/randomness.py:145-147);
-// counts >= 4 (2% of areas) finish in a loop over the shared table.
-__device__ __forceinline__ uint32_t poisson_count(uint64_t X, const PassParams &P,
+// Poisson(1) count of the area whose Poisson hash (stream 3, j = 0) is h:
+// #{m : (h >> 11) >= thr[m]} (inverse CDF, ref/randomness.py:145-147);
+// counts >= 6 (0.06 % of areas) finish in a loop over the shared table.
+__device__ __forceinline__ uint32_t poisson_count(uint64_t h, const PassParams &P,
                                                   const SmemTables &T) {
 #if DSK_PT_IMM
-  uint32_t c = (X >= kPt0) + (X >= kPt1) + (X >= kPt2) + (X >= kPt3);
+  uint32_t c = (h >= (kPt0 << 11)) + (h >= (kPt1 << 11)) + (h >= (kPt2 << 11)) +
+               (h >= (kPt3 << 11)) + (h >= (kPt4 << 11)) + (h >= (kPt5 << 11));
   (void)P;
+  if (c == 6) {
+    const uint64_t X = h >> 11;
+    while (X >= T.pthr[c]) c++;
+  }
 #else
+  const uint64_t X = h >> 11;
   uint32_t c = (X >= P.pt0) + (X >= P.pt1) + (X >= P.pt2) + (X >= P.pt3);
-#endif
   if (c == 4) {
     while (X >= T.pthr[c]) c++;
   }
+#endif
   return c;
 }
 
@@ -407,7 +417,7 @@ struct Engine {
   __device__ __forceinline__ void emit_area(bool valid, uint64_t pa, double x, uint32_t w,
                                             uint32_t r, uint32_t meta, bool lb, uint32_t elem) {
     if (!kFuse) {
-      const uint32_t k = poisson_count(finalize(pa ^ T.js[0][kStreamPoisson - 1]) >> 11, P, T);
+      const uint32_t k = poisson_count(finalize(pa ^ T.js[0][kStreamPoisson - 1]), P, T);
       const uint32_t cnt = valid ? k : 0;
       if (!lb) n_darts += cnt;
       push_area(cnt > 0, pa, x, w, r, meta | (cnt << 16), elem);
@@ -415,7 +425,7 @@ struct Engine {
     }
     const uint64_t hp = finalize(pa ^ T.js[0][kStreamPoisson - 1]);
     const uint64_t hu = finalize(pa ^ T.js[0][kStreamU - 1]);
-    const uint32_t k = poisson_count(hp >> 11, P, T);
+    const uint32_t k = poisson_count(hp, P, T);
     const uint32_t cnt = valid ? k : 0;
     if (!lb) n_darts += cnt;
     finish_dart(cnt > 0, pa, meta, w, r, x, 0, u53(hu), elem);
@@ -610,8 +620,7 @@ struct Engine {
     uint2 d = Q.elD[wk_slot];
     const int nu = wk_nu;
     const uint32_t r = wk_r;
-    uint64_t p = el.x ^ T.tNu[nu] ^ T.tRho[0] ^ T.tW[0][0] ^ T.tW[1][0] ^ T.cfold ^
-                 T.tR[0][r & 0xff] ^ T.tR[1][(r >> 8) & 0xff];
+    uint64_t p = el.x ^ T.tNu[nu] ^ T.dfold ^ T.tR[0][r & 0xff] ^ T.tR[1][(r >> 8) & 0xff];
     const bool hp = (wk_rlo & 0x80000000u) != 0;
     const bool lb = hp && r == (wk_rlo & 0x7fffffffu);
     const uint32_t meta = (uint32_t)nu | (nu >= (int)(d.y >> 8) ? kArWb : 0) |

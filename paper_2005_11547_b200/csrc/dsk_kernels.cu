@@ -160,6 +160,7 @@ __device__ void load_tables(SmemTables &T, const TableArgs &a) {
     uint64_t b = a.tab[20 * 256 + kStreamBucket] ^ a.tab[21 * 256];
     for (int p = 8; p < 20; p++) b ^= a.tab[p * 256];
     T.bconst = b;
+    T.dfold = a.tab[9 * 256] ^ a.tab[10 * 256] ^ a.tab[11 * 256] ^ T.cfold;
   }
 }
 
@@ -851,7 +852,8 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
   }
   pthr[63] = pthr[63] > (1ULL << 53) ? pthr[63] : (1ULL << 53);  // X < 2^53: loop sentinel
 #if DSK_PT_IMM
-  if (pthr[0] != kPt0 || pthr[1] != kPt1 || pthr[2] != kPt2 || pthr[3] != kPt3) {
+  if (pthr[0] != kPt0 || pthr[1] != kPt1 || pthr[2] != kPt2 || pthr[3] != kPt3 ||
+      pthr[4] != kPt4 || pthr[5] != kPt5) {
     delete c;
     return set_err(DSK_EUNSUPPORTED, "Poisson CDF differs from the reference's POISSON1_CDF");
   }

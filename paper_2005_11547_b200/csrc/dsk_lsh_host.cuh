@@ -37,7 +37,12 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   size_t team_bytes = align16((size_t)L * S * 16) + align16((size_t)cap * 16) +
                       align16((size_t)cap * 4) + align16((size_t)L * K * 8) +
                       (gc ? align16((size_t)3 * L * sizeof(unsigned)) + 16 : 0);
-  size_t need = (size_t)grid * teams * team_bytes;
+  // phi0 = 2 when every one of L >= 8 buckets rarely fills at phi = 1
+  // (P(all L buckets >= K) <= 0.63^L; cfg4: phi* = 2 or 3 for every set)
+  int phi0 = L >= 8 ? 2 : 1;
+  if (const char *e = getenv("DSK_LSH_PHI0")) phi0 = atoi(e) == 2 ? 2 : 1;
+  const size_t retry_off = (size_t)grid * teams * team_bytes;
+  size_t need = retry_off + (phi0 > 1 ? align16((size_t)n * 4) + 16 : 0);
   // hit buffers from the context's stream-ordered scratch pool
   std::lock_guard<std::mutex> lock(c->scratch_mu);
   int slot;
@@ -53,21 +58,47 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.normalize = normalize;
   const char *ex = getenv("DSK_LSH_EXACT");
   a.exact_sort = ex && atoi(ex) != 0; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
+  a.phi0 = phi0;
+  a.retry_rows = nullptr;
+  a.retry_n = nullptr;
+  const char *fr = getenv("DSK_LSH_FORCE_RETRY");
+  a.force_retry = fr && atoi(fr) != 0;
   a.md = make_mod((uint32_t)L); a.G = G; a.out_keys = out_keys; a.out_fps = out_fps;
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
   a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap; a.S = S;
   a.tabs = table_args(c, (double)t);
-  if (gc) {
-    lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);
-  } else {
-    switch (NW) {
-      case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
-      case 22: lsh_kernel<22><<<grid, 22 * 32, lsh_smem(L, G, NW), st>>>(a); break;
-      default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+  auto launch = [&]() {
+    if (gc) {
+      lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);
+    } else {
+      switch (NW) {
+        case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+        case 22: lsh_kernel<22><<<grid, 22 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+        default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+      }
     }
-  }
-  count_launch();
+    count_launch();
+  };
+  launch();
   CUDA_TRY(cudaGetLastError());
+  if (phi0 > 1) {
+    // rows whose (0, 2 / l1] first band failed are redone from phi = 1 (the
+    // reference's own stepping); normally none, and the retry launch exits
+    uint32_t *rows = (uint32_t *)((char *)scratch + retry_off);
+    unsigned *cnt = (unsigned *)((char *)rows + align16((size_t)n * 4));
+    CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned), st));
+    int cg = (int)((n + 255) / 256 < 2 * c->num_sms ? (n + 255) / 256 : 2 * c->num_sms);
+    lsh_retry_compact_kernel<<<cg, 256, 0, st>>>(status, n, rows, cnt);
+    count_launch();
+    unsigned long long *counter2 = c->d_counter + (c->next_slot.fetch_add(1) % kCounterSlots);
+    CUDA_TRY(cudaMemsetAsync(counter2, 0, sizeof(unsigned long long), st));
+    a.counter = counter2;
+    a.phi0 = 1;
+    a.retry_rows = rows;
+    a.retry_n = cnt;
+    launch();
+    CUDA_TRY(cudaGetLastError());
+  }
   return scratch_release(c, slot, st);
 }
 

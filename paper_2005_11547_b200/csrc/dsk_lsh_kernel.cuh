@@ -42,6 +42,10 @@ struct LshSink {
   const unsigned int *prev;  // cnt at the start of this band
   unsigned int *full;   // buckets holding >= K hits
   int *overflow;
+  // First band of a phi0 > 1 start: hits with rank <= L1 = fl(1 / l1) are
+  // also counted per bucket, cnt1 = prev + L, and buckets reaching K in
+  // full[1], to recover phi* = 1 and H(1).  L1 sits in the team block at
+  // full + 2 (< 0: no split in this band); nothing extra is held in registers.
 
   // Bands are rank-ordered, so a bucket that held >= K darts when this band
   // began can never take a dart of this band into its K smallest: those hits
@@ -49,6 +53,11 @@ struct LshSink {
   __device__ void hit(bool valid, const HitInfo &h, int lane) {
     if (valid) {
       const uint32_t bucket = mod_u32(h.bhash, md);
+      const double L1 = *reinterpret_cast<const double *>(full + 2);
+      if (L1 >= 0.0 && h.rank <= L1) {
+        if (atomicAdd(const_cast<unsigned int *>(prev) + md.d + bucket, 1u) == K - 1)
+          atomicAdd(full + 1, 1u);
+      }
       if (!(DSK_LSH_CLOSE && prev[bucket] >= K)) {
         const unsigned slot = atomicAdd(&cnt[bucket], 1u);
         if (slot == K - 1) atomicAdd(full, 1u);
@@ -80,6 +89,10 @@ struct LshArgs {
   int32_t L, K;
   int32_t normalize;
   int32_t exact_sort;  // 1: skip the float-key fast path (env DSK_LSH_EXACT=1; tests)
+  int32_t phi0;        // first band (0, phi0 / l1]; 2 when phi* = 1 is unlikely (large L)
+  const uint32_t *retry_rows;  // second launch: rows whose first band failed (phi0 = 1)
+  const unsigned *retry_n;
+  int32_t force_retry;  // tests (env DSK_LSH_FORCE_RETRY=1): every first band is handed back
   double tf, inv_t;
   ModU32 md;
   int G;
@@ -139,7 +152,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   unsigned char *cb = kGC ? gs + o_cnt : tb + kTeamCtlBytes;
   unsigned int *cnt = reinterpret_cast<unsigned int *>(cb);
   unsigned int *off = cnt + L;
-  unsigned int *cur = off + L;
+  unsigned int *cnt1 = off + L;  // hits with rank <= fl(1 / l1), first band of a phi0 = 2 start
   unsigned int *fullc =
       reinterpret_cast<unsigned int *>(cb + align16((size_t)3 * L * sizeof(unsigned)));
   ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
@@ -164,16 +177,22 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   sink.overflow = &C.overflow;
 
   for (;;) {
-    if (tt == 0) C.set = (long long)atomicAdd(a.counter, 1ULL);
+    if (tt == 0) {
+      long long q = (long long)atomicAdd(a.counter, 1ULL);
+      if (a.retry_rows)  // retry launch: the rows the first launch handed back
+        q = q < (long long)*a.retry_n ? (long long)a.retry_rows[q] : a.n;
+      C.set = q;
+    }
     team_sync(G, team);
     const long long s = C.set;
     if (s >= a.n) break;
     const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
-    for (int i = tt; i < L; i += G * 32) cnt[i] = off[i] = 0;
+    for (int i = tt; i < L; i += G * 32) cnt[i] = off[i] = cnt1[i] = 0;
     if (tt == 0) {
       C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0;
       C.areas[0] = C.areas[1] = 0.0; C.chunk[0] = C.chunk[1] = 0;
-      C.darts = 0; C.hits = 0; C.total = 0; C.sexp = 0; C.overflow = 0; *fullc = 0;
+      C.darts = 0; C.hits = 0; C.total = 0; C.sexp = 0; C.overflow = 0;
+      fullc[0] = fullc[1] = 0;
     }
     team_sync(G, team);
     if (wit == 0)
@@ -188,42 +207,75 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       const double l1 = C.l1;
       const int maxd = C.maxdepth;
       const int sexp = C.sexp;
+      // The first band is (0, phi0 / l1]: the keys do not depend on the phi
+      // schedule, and counting the hits with
+      // rank <= fl(1 / l1) per bucket recovers phi* = 1.  A first band that
+      // fails (limit, depth or area cap at phi0 that phi = 1 might not hit)
+      // is redone from phi = 1 by a second launch, stepping exactly as the
+      // reference does.
+      const int phi0 = a.phi0;
       status = DSK_NOCONV;
       double L_prev = -1.0;
       int RD_prev = 0;
-      for (int phi = 1; phi <= 64; phi++) {  // ref/annindex.py:70
+      for (int phi = phi0; phi <= 64; phi++) {  // ref/annindex.py:70
+        int err = 0;
         double Lim = __ddiv_rn((double)phi, l1);
-        if (!(Lim > 0.0) || isinf(Lim)) { status = DSK_LIMIT; break; }
-        int RD = floor_log2_host(__dadd_rn(1.0, Lim), T.l2thr);
-        if (depth_status(maxd, RD)) { status = depth_status(maxd, RD); break; }
-        PassParams P;
-        P.gtab = a.tabs.tab;
-        P.inv_t = a.inv_t;
-        P.tf = a.tf;
-        P.L_hi = Lim;
-        P.L_lo = L_prev;
-        P.RD = RD;
-        P.RD_lo = RD_prev;
-        P.maxd = maxd;
-        poisson_regs(P, T);
-        const int par = phi & 1;
-        run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
-                 par, sexp);
-        team_sync(G, team);
-        const double areas = C.areas[par];
-        const bool ab = C.abort != 0;
-        const unsigned full = *fullc;
-        const bool ovf = C.overflow != 0;
-        if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
-        for (int i = tt; i < L; i += G * 32) off[i] = cnt[i];  // band snapshot
-        team_sync(G, team);
-        if (ab || areas > kMaxAreas) { status = DSK_AREAS; break; }  // ref/darthash.py:243
-        if (ovf) { status = DSK_SCRATCH; break; }
-        final_areas = areas;
-        // ref/annindex.py:72-76: >= L*K darts and every bucket >= K
-        if (full == (unsigned)L) {  // implies >= L*K darts
-          status = DSK_OK;
-          phi_star = phi;
+        int RD = 0;
+        if (!(Lim > 0.0) || isinf(Lim)) {
+          err = DSK_LIMIT;
+        } else {
+          RD = floor_log2_host(__dadd_rn(1.0, Lim), T.l2thr);
+          err = depth_status(maxd, RD);
+        }
+        if (!err) {
+          PassParams P;
+          P.gtab = a.tabs.tab;
+          P.inv_t = a.inv_t;
+          P.tf = a.tf;
+          P.L_hi = Lim;
+          P.L_lo = L_prev;
+          P.RD = RD;
+          P.RD_lo = RD_prev;
+          P.maxd = maxd;
+          poisson_regs(P, T);
+          const int par = phi & 1;
+          if (tt == 0)
+            *reinterpret_cast<double *>(fullc + 2) =
+                (phi == phi0 && phi0 > 1) ? __ddiv_rn(1.0, l1) : -1.0;
+          team_sync(G, team);
+          run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
+                   par, sexp);
+          team_sync(G, team);
+          const double areas = C.areas[par];
+          const bool ab = C.abort != 0;
+          const unsigned full = fullc[0], full1 = fullc[1];
+          const bool ovf = C.overflow != 0;
+          if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
+          for (int i = tt; i < L; i += G * 32) off[i] = cnt[i];  // band snapshot
+          team_sync(G, team);
+          if (ab || areas > kMaxAreas) err = DSK_AREAS;  // ref/darthash.py:243
+          else if (ovf) err = DSK_SCRATCH;
+          else if (a.force_retry && phi == phi0 && phi0 > 1) err = DSK_RETRY;  // tests
+          if (!err) {
+            final_areas = areas;
+            // ref/annindex.py:72-76: >= L*K darts and every bucket >= K
+            if (full == (unsigned)L) {  // implies >= L*K darts
+              status = DSK_OK;
+              phi_star = phi;
+              if (phi == phi0 && phi0 > 1 && full1 == (unsigned)L) {
+                phi_star = 1;  // H(1) = the hits counted below fl(1 / l1)
+                n_hits = 0;
+                if (wit == 0)
+                  for (int i = lane; i < L; i += 32) n_hits += cnt1[i];
+              }
+              break;
+            }
+          }
+        }
+        if (err) {
+          // a failing first band at phi0 > 1: the host's retry launch redoes
+          // the set from phi = 1 (dsk_lsh_csr)
+          status = (phi == phi0 && phi0 > 1) ? DSK_RETRY : err;
           break;
         }
         L_prev = Lim;
@@ -426,3 +478,12 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   }
 }
 
+
+// Rows of a phi0 = 2 launch whose first band failed (DSK_RETRY), for the
+// retry launch that redoes them from phi = 1.
+__global__ void lsh_retry_compact_kernel(const int32_t *status, int64_t n, uint32_t *rows,
+                                         unsigned *count) {
+  for (int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; r < n;
+       r += (int64_t)gridDim.x * blockDim.x)
+    if (status[r] == DSK_RETRY) rows[atomicAdd(count, 1u)] = (uint32_t)r;
+}

@@ -256,3 +256,30 @@ def test_bits_only_tie_resolution():
     api._resolve_minhash_ties(res, p, i, ww, 256, f, dev)
     assert np.array_equal(as_u64(res.bits), good)
     assert (res.status.cpu().numpy() == 0).all()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("mode", ["phi0=1", "phi0=2", "retry"])
+@pytest.mark.parametrize("L,K", [(100, 20), (8, 1), (2, 3)])
+def test_lsh_first_band_schedules(monkeypatch, mode, L, K):
+    """The LSH kernel's first band (0, phi0 / l1] (phi0 = 2 for L >= 8), its
+    phi* = 1 recovery, and the retry launch from phi = 1 all give the
+    oracle's keys, fingerprints, phi* and H(phi*) (ref/annindex.py:64-82)."""
+    from paper_2005_11547_b200 import HashFamily, LshParams, as_u64, lsh_batch
+    if mode == "phi0=1":
+        monkeypatch.setenv("DSK_LSH_PHI0", "1")
+    elif mode == "phi0=2":
+        monkeypatch.setenv("DSK_LSH_PHI0", "2")
+    else:
+        monkeypatch.setenv("DSK_LSH_PHI0", "2")
+        monkeypatch.setenv("DSK_LSH_FORCE_RETRY", "1")
+    indptr, ids, w = workloads.generate("cfg4", n=400, start=3000)
+    res = lsh_batch(indptr, ids, w, LshParams(L, K), HashFamily(3), fps=True)
+    keys, fps, status, phi, hits = Oracle(3).lsh_csr(indptr, ids, w, L, K, want_fps=True)
+    assert (status == 0).all() and (res.status.cpu().numpy() == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(as_u64(res.fps), fps)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+    assert np.array_equal(res.stats.cpu().numpy()[:, 2], hits)
+    if (L, K) == (2, 3):
+        assert (phi == 1).any()  # the phi* = 1 recovery is exercised
