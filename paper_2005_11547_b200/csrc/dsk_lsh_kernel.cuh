@@ -302,7 +302,57 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         const unsigned nb = cnt[b];
         const size_t o = (size_t)b * S;  // bucket b's slots (nb <= 64 <= S on the register paths)
         bool exact = nb > 64 || DSK_LSH_FAST == 0 || a.exact_sort;
-        if (!exact) {
+        if (!exact && K <= 32) {
+          // fast path: bitonic sort of the 32-bit float-rounded ranks (float
+          // rounding is monotone); when the first K + 1 sorted keys are
+          // distinct, their order and the K-set equal the exact (rank, fp)
+          // order, and each entry finds its own position by a 5-step binary
+          // search over the sorted first 32 keys.  Otherwise the bucket takes
+          // the exact path below.
+          uint32_t key[2], own[2];
+#pragma unroll
+          for (int h = 0; h < 2; h++) {
+            unsigned i = lane + 32 * h;
+            own[h] = i < nb ? __float_as_uint(__double2float_rn(
+                                  __longlong_as_double((long long)buf[o + i].y)))
+                            : 0xffffffffu;  // above every float bit pattern of a rank
+            key[h] = own[h];
+          }
+          for (int kk = 2; kk <= 64; kk <<= 1) {
+            for (int j = kk >> 1; j > 0; j >>= 1) {
+              if (j == 32) {
+                if (key[1] < key[0]) { uint32_t t0 = key[0]; key[0] = key[1]; key[1] = t0; }
+              } else {
+#pragma unroll
+                for (int h = 0; h < 2; h++) {
+                  int p = lane + 32 * h;
+                  uint32_t y = __shfl_xor_sync(DSK_FULL, key[h], j);
+                  bool take_min = ((p & j) == 0) == ((p & kk) == 0);
+                  if (take_min == (y < key[h])) key[h] = y;
+                }
+              }
+            }
+          }
+          // positions 0..K (K <= 32: lanes 0..K of key[0], position 32 = lane 0 of key[1])
+          uint32_t nx = __shfl_down_sync(DSK_FULL, key[0], 1);
+          uint32_t f1 = __shfl_sync(DSK_FULL, key[1], 0);
+          if (lane == 31) nx = f1;
+          const bool coll = (unsigned)lane < (unsigned)K && (unsigned)lane + 1 < nb && nx == key[0];
+          exact = __any_sync(DSK_FULL, coll) && DSK_LSH_FAST == 1;
+          if (!exact) {
+#pragma unroll
+            for (int h = 0; h < 2; h++) {
+              unsigned pos = 0;  // #{sorted first-32 keys < own}
+#pragma unroll
+              for (int step = 16; step >= 1; step >>= 1) {
+                uint32_t v = __shfl_sync(DSK_FULL, key[0], (int)pos + step - 1);
+                if (v < own[h]) pos += step;
+              }
+              unsigned i = lane + 32 * h;
+              if (i < nb && pos < (unsigned)K) sel[(size_t)b * K + pos] = buf[o + i].x;
+            }
+          }
+        } else if (!exact) {
           // fast path: bitonic sort of one 64-bit key per entry, the rank
           // rounded to float (monotone) above the entry's buffer index; when
           // the first K + 1 sorted keys have distinct float ranks their order
