@@ -123,102 +123,94 @@ __device__ __forceinline__ int64_t weight_window(double x, double w0, double dnu
 }
 
 // numpy pairwise summation (pairwise_sum_DOUBLE, PW_BLOCKSIZE 128), i.e.
-// float(np.sum(weights)) of ref/core.py:44.  Leaf of the recursion:
-// (`sexp` != 0 sums the values rescaled by 2^sexp, i.e. np.sum(np.ldexp(a, sexp)).)
+// float(np.sum(weights)) of ref/core.py:44, warp-cooperative and without
+// local memory.  (`sexp` != 0 sums the values rescaled by 2^sexp, i.e.
+// np.sum(np.ldexp(a, sexp)).)
+//
+// numpy's recursion on n elements: n < 8 -> sequential sum; n <= 128 ->
+// eight strided accumulators r[j] = a[j] + a[j+8] + ... (sequential per j),
+// combined as ((r0+r1)+(r2+r3))+((r4+r5)+(r6+r7)), then the n % 8 tail
+// added in order; otherwise split at n2 = n/2 - (n/2 mod 8) and add the two
+// halves' sums.
 __device__ __forceinline__ double pw_ld(const double *a, int64_t i, int sexp) {
   return sexp ? scalbn(a[i], sexp) : a[i];
 }
 
-__device__ __forceinline__ double pw_leaf(const double *a, int64_t n, int sexp) {
+// A leaf (n <= 128) of the recursion, by the whole warp: lane j < 8 runs
+// accumulator j's chain; the result is returned to every lane.
+__device__ __forceinline__ double warp_pw_leaf(const double *a, int64_t n, int lane, int sexp) {
+  double res = 0.0;
   if (n < 8) {
-    double res = 0.0;
-    for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, pw_ld(a, i, sexp));
-    return res;
+    if (lane == 0)
+      for (int64_t i = 0; i < n; i++) res = __dadd_rn(res, pw_ld(a, i, sexp));
+    return __shfl_sync(DSK_FULL, res, 0);
   }
-  double r[8];
+  const int64_t body = n - (n % 8);
+  double r = 0.0;
+  if (lane < 8) {
+    double v[16];  // <= 16 terms per chain (n <= 128); loads first, then the in-order adds
 #pragma unroll
-  for (int j = 0; j < 8; j++) r[j] = pw_ld(a, j, sexp);
-  int64_t i;
-  for (i = 8; i < n - (n % 8); i += 8) {
+    for (int q = 0; q < 16; q++) v[q] = 8 * q + lane < body ? pw_ld(a, 8 * q + lane, sexp) : 0.0;
+    r = v[0];
 #pragma unroll
-    for (int j = 0; j < 8; j++) r[j] = __dadd_rn(r[j], pw_ld(a, i + j, sexp));
+    for (int q = 1; q < 16; q++)
+      if (8 * q + lane < body) r = __dadd_rn(r, v[q]);
   }
-  double res = __dadd_rn(__dadd_rn(__dadd_rn(r[0], r[1]), __dadd_rn(r[2], r[3])),
-                         __dadd_rn(__dadd_rn(r[4], r[5]), __dadd_rn(r[6], r[7])));
-  for (; i < n; i++) res = __dadd_rn(res, pw_ld(a, i, sexp));
-  return res;
+  // ((r0 + r1) + (r2 + r3)) + ((r4 + r5) + (r6 + r7)): pairs at distance 1, 2, 4
+  r = __dadd_rn(r, __shfl_down_sync(DSK_FULL, r, 1));
+  r = __dadd_rn(r, __shfl_down_sync(DSK_FULL, r, 2));
+  r = __dadd_rn(r, __shfl_down_sync(DSK_FULL, r, 4));
+  if (lane == 0)
+    for (int64_t i = body; i < n; i++) r = __dadd_rn(r, pw_ld(a, i, sexp));
+  return __shfl_sync(DSK_FULL, r, 0);
 }
 
-// Post-order evaluation of the pairwise recursion over n > 128 elements.
-// Leaf values come from `leaf(start, len, index)`.
-template <class LeafFn>
-__device__ double pw_combine(int64_t n, LeafFn leaf) {
-  // explicit stack: (start, len, state, left)
-  int64_t st_start[48], st_len[48];
-  double st_left[48];
-  int st_state[48];
-  int sp = 0;
-  int64_t leaf_idx = 0;
+// Warp-cooperative float(np.sum(a)) for any n.  The recursion is walked in
+// post order by the whole warp (warp-uniform control flow); its stack lives
+// in registers across the lanes -- lane d holds the node at depth d (start,
+// length, state, left sum) -- so nothing spills to local memory.  Depth <=
+// log2(n / 64) + 1 < 32 for every n < 2^31.  (`scratch` is unused; kept for
+// the callers' signature.)
+__device__ __forceinline__ double warp_np_sum(const double *a, int64_t n, double *scratch,
+                                           int lane, int sexp) {
+  (void)scratch;
+  if (n <= 128) return warp_pw_leaf(a, n, lane, sexp);
+  int64_t nstart = 0, nlen = n;  // this lane's stack entry
+  int nstate = 0;                // 0 fresh, 1 left child pending, 2 right child pending
+  double nleft = 0.0;
+  int sp = 1;                    // warp-uniform stack depth; lane 0 holds the root
   double ret = 0.0;
-  st_start[0] = 0; st_len[0] = n; st_state[0] = 0; sp = 1;
   while (sp > 0) {
-    int top = sp - 1;
-    int64_t len = st_len[top];
+    const int top = sp - 1;
+    const int64_t len = __shfl_sync(DSK_FULL, nlen, top);
+    const int64_t start = __shfl_sync(DSK_FULL, nstart, top);
     if (len <= 128) {
-      ret = leaf(st_start[top], len, leaf_idx++);
+      ret = warp_pw_leaf(a + start, len, lane, sexp);
       sp--;
-      // deliver to parent
-      while (sp > 0) {
-        int p = sp - 1;
-        if (st_state[p] == 1) {  // left child returned
-          st_left[p] = ret;
-          st_state[p] = 2;
-          int64_t n2 = st_len[p] / 2;
+      while (sp > 0) {  // deliver to the parents
+        const int p = sp - 1;
+        if (__shfl_sync(DSK_FULL, nstate, p) == 1) {  // left child returned: push the right
+          const int64_t plen = __shfl_sync(DSK_FULL, nlen, p);
+          const int64_t pstart = __shfl_sync(DSK_FULL, nstart, p);
+          int64_t n2 = plen / 2;
           n2 -= n2 % 8;
-          st_start[sp] = st_start[p] + n2; st_len[sp] = st_len[p] - n2; st_state[sp] = 0;
+          if (lane == p) { nleft = ret; nstate = 2; }
+          if (lane == sp) { nstart = pstart + n2; nlen = plen - n2; nstate = 0; }
           sp++;
           break;
-        } else {  // right child returned
-          ret = __dadd_rn(st_left[p], ret);
-          sp--;
         }
+        ret = __dadd_rn(__shfl_sync(DSK_FULL, nleft, p), ret);  // right child returned
+        sp--;
       }
     } else {
       int64_t n2 = len / 2;
       n2 -= n2 % 8;
-      st_state[top] = 1;
-      st_start[sp] = st_start[top]; st_len[sp] = n2; st_state[sp] = 0;
+      if (lane == top) nstate = 1;
+      if (lane == sp) { nstart = start; nlen = n2; nstate = 0; }
       sp++;
     }
   }
   return ret;
-}
-
-// Warp-cooperative float(np.sum(a)): leaves (<=128 elements) are summed by
-// the lanes in parallel, lane 0 combines them in the recursion's order.
-// `scratch` holds >= 256 doubles of warp-private shared memory.
-__device__ __forceinline__ double warp_np_sum(const double *a, int64_t n, double *scratch,
-                                              int lane, int sexp) {
-  double s = 0.0;
-  if (n <= 128) {
-    if (lane == 0) s = pw_leaf(a, n, sexp);
-    return __shfl_sync(DSK_FULL, s, 0);
-  }
-  if (n <= 256 * 64) {  // leaves are longer than 64 elements: < 256 of them
-    pw_combine(n, [&](int64_t start, int64_t len, int64_t idx) {
-      if ((idx & 31) == lane) scratch[idx] = pw_leaf(a + start, len, sexp);
-      return 0.0;
-    });
-    __syncwarp();
-    if (lane == 0)
-      s = pw_combine(n, [&](int64_t, int64_t, int64_t idx) { return scratch[idx]; });
-  } else if (lane == 0) {
-    s = pw_combine(n, [&](int64_t start, int64_t len, int64_t) {
-      return pw_leaf(a + start, len, sexp);
-    });
-  }
-  __syncwarp();
-  return __shfl_sync(DSK_FULL, s, 0);
 }
 
 // x mod d for 64-bit x, 32-bit d >= 1 (bucket_array's uint64 %, ref/randomness.py:219)

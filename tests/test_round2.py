@@ -283,3 +283,20 @@ def test_lsh_first_band_schedules(monkeypatch, mode, L, K):
     assert np.array_equal(res.stats.cpu().numpy()[:, 2], hits)
     if (L, K) == (2, 3):
         assert (phi == 1).any()  # the phi* = 1 recovery is exercised
+
+
+@pytest.mark.gpu
+def test_l1_pairwise_all_small_and_deep_sizes():
+    """The register-stack numpy pairwise sum (warp_np_sum) equals np.sum for
+    every length 0..300, random lengths up to 7e4 and a 2^20 + 13 row (a
+    deep recursion), with weights spread over 2^+-20."""
+    from paper_2005_11547_b200 import l1_batch
+    rng = np.random.default_rng(11)
+    sizes = list(range(0, 301)) + rng.integers(301, 70000, 40).tolist() + [2**20 + 13]
+    lens = np.array(sizes, dtype=np.int64)
+    indptr = np.zeros(lens.size + 1, dtype=np.int64)
+    np.cumsum(lens, out=indptr[1:])
+    w = rng.lognormal(0.0, 7.0, int(indptr[-1]))
+    got = l1_batch(indptr, w).cpu().numpy()
+    exp = np.array([float(np.sum(w[indptr[s]:indptr[s + 1]])) for s in range(lens.size)])
+    assert np.array_equal(got, exp)
