@@ -76,3 +76,66 @@ def test_gather_rows_gloo(world):
     for p in procs:
         p.join(timeout=60)
     assert all(ok for _, ok in res), res
+
+
+def _rank_rows_worker(rank, world, port, q, use_gpu):
+    """bench.py's strong-scaling data path: plan from row lengths alone, each
+    rank generates only its own rows; with use_gpu the rows are sketched on
+    the (shared) GPU and the outputs gathered over gloo."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    n = 20000
+    lens = workloads.lengths("cfg5", n)
+    bounds = shard.plan_shards_lengths(lens, world, 750)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    p, i, w = workloads.generate("cfg5", n=r1 - r0, start=r0, workers=2)
+    if use_gpu:
+        from paper_2005_11547_b200 import HashFamily, minhash_batch
+        res = minhash_batch(p, i, w, 128, HashFamily(4), bits=True, device="cuda:0")
+        local = torch.cat([res.values, res.bits, res.status.to(torch.int64).unsqueeze(1)],
+                          dim=1).cpu()
+    else:
+        local = torch.from_numpy(np.stack([np.diff(p), np.add.reduceat(w.view(np.int64), p[:-1])],
+                                          axis=1)) if r1 > r0 else torch.zeros((0, 2), torch.int64)
+    full = shard.gather_rows(local, bounds)
+    if rank == 0:
+        fp, fi, fw = workloads.generate("cfg5", n=n, workers=2)
+        if use_gpu:
+            res = minhash_batch(fp, fi, fw, 128, HashFamily(4), bits=True, device="cuda:0")
+            one = torch.cat([res.values, res.bits, res.status.to(torch.int64).unsqueeze(1)],
+                            dim=1).cpu()
+        else:
+            one = torch.from_numpy(np.stack([np.diff(fp),
+                                             np.add.reduceat(fw.view(np.int64), fp[:-1])], axis=1))
+        q.put((rank, bool(torch.equal(full, one))))
+    else:
+        q.put((rank, True))
+    dist.destroy_process_group()
+
+
+def _run_ranks(world, use_gpu):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rank_rows_worker, args=(r, world, port, q, use_gpu))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
+def test_rank_local_generation_gloo():
+    """Per-rank generation over a lengths-only plan reproduces the one-process rows."""
+    _run_ranks(2, use_gpu=False)
+
+
+@pytest.mark.gpu
+def test_rank_shards_byte_identical_to_one_launch_gloo():
+    """Two ranks (gloo, sharing the one GPU; their kernels never wait on each
+    other) sketch their own cfg5 row ranges; the gathered values, 1-bit words
+    and statuses are byte-identical to a single launch over all rows."""
+    _run_ranks(2, use_gpu=True)
