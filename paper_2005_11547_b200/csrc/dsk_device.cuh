@@ -281,6 +281,12 @@ __device__ __forceinline__ void ld128_shared(const uint64_t *addr, uint64_t &lo,
   asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(a) : "memory");
 }
 
+// Invalidate one 128-byte L2 line (128-byte aligned) without writing it back:
+// for scratch whose contents are dead, so dirty lines never reach HBM.
+__device__ __forceinline__ void l2_discard(const void *line) {
+  asm volatile("discard.global.L2 [%0], 128;" ::"l"(line) : "memory");
+}
+
 // generic-address forms (slot arrays in global memory for large k)
 __device__ __forceinline__ void cas128_generic(uint64_t *addr, uint64_t cmp_lo, uint64_t cmp_hi,
                                                uint64_t val_lo, uint64_t val_hi, uint64_t &old_lo,

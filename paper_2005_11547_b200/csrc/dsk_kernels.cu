@@ -165,6 +165,7 @@ __device__ void load_tables(SmemTables &T, const TableArgs &a) {
 }
 
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+__host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~(size_t)127; }
 
 constexpr size_t kOffQueues = align16(sizeof(SmemTables));
 constexpr size_t kQBytes = align16(sizeof(WarpQueues));

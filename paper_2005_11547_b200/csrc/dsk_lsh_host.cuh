@@ -30,13 +30,14 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   S64 = S64 < 64 ? 64 : (S64 + 31) / 32 * 32;
   if (S64 > (1 << 20)) S64 = 1 << 20;
   if (const char *e = getenv("DSK_LSH_SLOTS"))  // tests: force the overflow list
-    S64 = atoi(e) > 64 ? atoi(e) : 64;
+    S64 = atoi(e) > 64 ? (atoi(e) + 7) / 8 * 8 : 64;  // 128-byte bucket regions
   const uint32_t S = (uint32_t)S64;
   // overflow list per team for buckets past their S slots (rare)
   uint32_t cap = (uint32_t)(2 * t > 16384 ? (2 * t < (1 << 26) ? 2 * t : (1 << 26)) : 16384);
-  size_t team_bytes = align16((size_t)L * S * 16) + align16((size_t)cap * 16) +
-                      align16((size_t)cap * 4) + align16((size_t)L * K * 8) +
-                      (gc ? align16((size_t)3 * L * sizeof(unsigned)) + 16 : 0);
+  // 128-byte aligned regions (the kernel discards spent lines; lsh_kernel's layout)
+  size_t team_bytes = align128((size_t)L * S * 16) + align128((size_t)cap * 16) +
+                      align128((size_t)cap * 4) + align128((size_t)L * K * 8) +
+                      (gc ? align128(align16((size_t)3 * L * sizeof(unsigned)) + 16) : 0);
   // phi0 = 2 when every one of L >= 8 buckets rarely fills at phi = 1
   // (P(all L buckets >= K) <= 0.63^L; cfg4: phi* = 2 or 3 for every set)
   int phi0 = L >= 8 ? 2 : 1;

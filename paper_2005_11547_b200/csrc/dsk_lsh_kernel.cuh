@@ -2,6 +2,9 @@
 #ifndef DSK_LSH_CLOSE
 #define DSK_LSH_CLOSE 1  // drop hits of buckets already full when the band began
 #endif
+#ifndef DSK_LSH_DISCARD
+#define DSK_LSH_DISCARD 1  // discard spent hit-slot / selection lines from L2 (no write-back)
+#endif
 #ifndef DSK_LSH_FAST
 #define DSK_LSH_FAST 1  // 0: exact sort only; 1: float-key sort + exact fallback; 2: timing only
 #endif
@@ -145,10 +148,11 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
 #else
   unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
 #endif
-  // team scratch: slots L*S*16 | overflow cap*16 | overflow buckets cap*4 |
-  // selection L*K*8 | (kGC) counters
-  const size_t o_ovf = align16((size_t)L * a.S * 16), o_ovb = o_ovf + align16((size_t)a.cap * 16);
-  const size_t o_sel = o_ovb + align16((size_t)a.cap * 4), o_cnt = o_sel + align16((size_t)L * K * 8);
+  // team scratch (128-byte aligned regions, so spent lines can be discarded):
+  // slots L*S*16 | overflow cap*16 | overflow buckets cap*4 | selection
+  // L*K*8 | (kGC) counters
+  const size_t o_ovf = align128((size_t)L * a.S * 16), o_ovb = o_ovf + align128((size_t)a.cap * 16);
+  const size_t o_sel = o_ovb + align128((size_t)a.cap * 4), o_cnt = o_sel + align128((size_t)L * K * 8);
   unsigned char *cb = kGC ? gs + o_cnt : tb + kTeamCtlBytes;
   unsigned int *cnt = reinterpret_cast<unsigned int *>(cb);
   unsigned int *off = cnt + L;
@@ -480,6 +484,12 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
             if (pos < (unsigned)K) sel[(size_t)b * K + pos] = e.x;
           }
         }
+        // the bucket's slots are spent: drop their L2 lines without a write-back
+        // (the next set rewrites them), so the hit buffer never round-trips to HBM
+#if DSK_LSH_DISCARD
+        const unsigned lines = ((nb < S ? nb : S) * 16 + 127) / 128;
+        for (unsigned q = lane; q < lines; q += 32) l2_discard(buf + o + 8 * q);
+#endif
       }
       if (__any_sync(DSK_FULL, tie) && lane == 0) atomicOr(&C.tie, 1);
       __threadfence_block();
@@ -505,6 +515,11 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         }
         if (a.out_keys) a.out_keys[(size_t)s * L + b] = mixed;
       }
+#if DSK_LSH_DISCARD
+      team_sync(G, team);  // every table's selection has been read
+      const unsigned sel_lines = ((unsigned)L * K * 8 + 127) / 128;
+      for (unsigned q = tt; q < sel_lines; q += G * 32) l2_discard(sel + 16 * q);
+#endif
     } else {
       for (int b = tt; b < L; b += G * 32) {
         if (a.out_keys) a.out_keys[(size_t)s * L + b] = 0;

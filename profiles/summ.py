@@ -3,8 +3,9 @@ import csv, subprocess, sys
 rep = sys.argv[1]
 out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(out.splitlines()))
-hdr, val = rows[0], rows[2]
+hdr, units, val = rows[0], rows[1], rows[2]
 d = dict(zip(hdr, val))
+u = dict(zip(hdr, units))
 keys = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__inst_executed.avg.per_cycle_active",
         "smsp__issue_active.avg.pct_of_peak_sustained_active", "smsp__warps_active.avg.per_cycle_active",
         "smsp__warps_eligible.avg.per_cycle_active", "launch__registers_per_thread",
@@ -16,7 +17,7 @@ keys = ["gpu__time_duration.sum", "smsp__inst_executed.sum", "sm__inst_executed.
         "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum",
         "dram__bytes_read.sum", "dram__bytes_write.sum"]
 for k in keys:
-    print(f"{k:70s} {d.get(k)}")
+    print(f"{k:70s} {d.get(k)} {u.get(k, '')}")
 st = []
 for k in hdr:
     if k.startswith("smsp__average_warps_issue_stalled_") and k.endswith("_per_issue_active.ratio"):
