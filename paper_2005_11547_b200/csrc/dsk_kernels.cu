@@ -885,12 +885,6 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
-  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24, false, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
-  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<22, false, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
-  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20, false, true>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   *out = c;
   return DSK_OK;
 }

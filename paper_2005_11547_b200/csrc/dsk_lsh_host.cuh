@@ -42,18 +42,8 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   // (P(all L buckets >= K) <= 0.63^L; cfg4: phi* = 2 or 3 for every set)
   int phi0 = L >= 8 ? 2 : 1;
   if (const char *e = getenv("DSK_LSH_PHI0")) phi0 = atoi(e) == 2 ? 2 : 1;
-  const char *ex = getenv("DSK_LSH_EXACT");
-  const bool exact_sort = ex && atoi(ex) != 0;
-  // compact 12-byte hit slots (fingerprint + float rank) keep a launch's hit
-  // buffers in L2; sets needing exact ranks go to the exact retry launch
-  bool compact = !gc && K <= 32 && !exact_sort;
-  if (const char *e = getenv("DSK_LSH_COMPACT")) compact = compact && atoi(e) != 0;
-  const size_t compact_bytes =
-      lsh_compact_scratch(L, S) + (gc ? align128(align16((size_t)3 * L * sizeof(unsigned)) + 16) : 0);
-  const size_t stride = compact && compact_bytes > team_bytes ? compact_bytes : team_bytes;
-  const size_t retry_off = (size_t)grid * teams * stride;
-  const bool retry = phi0 > 1 || compact;
-  size_t need = retry_off + (retry ? align16((size_t)n * 4) + 16 : 0);
+  const size_t retry_off = (size_t)grid * teams * team_bytes;
+  size_t need = retry_off + (phi0 > 1 ? align16((size_t)n * 4) + 16 : 0);
   // hit buffers from the context's stream-ordered scratch pool
   std::lock_guard<std::mutex> lock(c->scratch_mu);
   int slot;
@@ -67,7 +57,8 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   LshArgs a;
   a.indptr = indptr; a.ids = ids; a.w = weights; a.n = n; a.L = L; a.K = K;
   a.normalize = normalize;
-  a.exact_sort = exact_sort; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
+  const char *ex = getenv("DSK_LSH_EXACT");
+  a.exact_sort = ex && atoi(ex) != 0; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
   a.phi0 = phi0;
   a.retry_rows = nullptr;
   a.retry_n = nullptr;
@@ -75,35 +66,25 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.force_retry = fr && atoi(fr) != 0;
   a.md = make_mod((uint32_t)L); a.G = G; a.out_keys = out_keys; a.out_fps = out_fps;
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
-  a.scratch = (unsigned char *)scratch; a.team_scratch = compact ? compact_bytes : team_bytes;
-  a.cap = cap; a.S = S;
+  a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap; a.S = S;
   a.tabs = table_args(c, (double)t);
-  auto launch = [&](bool cmp) {
-    const size_t sm = lsh_smem(L, G, NW);
+  auto launch = [&]() {
     if (gc) {
       lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);
-    } else if (cmp) {
-      switch (NW) {
-        case 24: lsh_kernel<24, false, true><<<grid, 24 * 32, sm, st>>>(a); break;
-        case 22: lsh_kernel<22, false, true><<<grid, 22 * 32, sm, st>>>(a); break;
-        default: lsh_kernel<20, false, true><<<grid, 20 * 32, sm, st>>>(a); break;
-      }
     } else {
       switch (NW) {
-        case 24: lsh_kernel<24><<<grid, 24 * 32, sm, st>>>(a); break;
-        case 22: lsh_kernel<22><<<grid, 22 * 32, sm, st>>>(a); break;
-        default: lsh_kernel<20><<<grid, 20 * 32, sm, st>>>(a); break;
+        case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+        case 22: lsh_kernel<22><<<grid, 22 * 32, lsh_smem(L, G, NW), st>>>(a); break;
+        default: lsh_kernel<20><<<grid, 20 * 32, lsh_smem(L, G, NW), st>>>(a); break;
       }
     }
     count_launch();
   };
-  launch(compact);
+  launch();
   CUDA_TRY(cudaGetLastError());
-  if (retry) {
-    // rows handed back by the first launch -- a (0, 2 / l1] first band that
-    // failed, or a compact selection that needs exact ranks -- are redone from
-    // phi = 1 with exact hit slots (the reference's own stepping); normally
-    // none or a few, and the retry launch exits at once
+  if (phi0 > 1) {
+    // rows whose (0, 2 / l1] first band failed are redone from phi = 1 (the
+    // reference's own stepping); normally none, and the retry launch exits
     uint32_t *rows = (uint32_t *)((char *)scratch + retry_off);
     unsigned *cnt = (unsigned *)((char *)rows + align16((size_t)n * 4));
     CUDA_TRY(cudaMemsetAsync(cnt, 0, sizeof(unsigned), st));
@@ -116,8 +97,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     a.phi0 = 1;
     a.retry_rows = rows;
     a.retry_n = cnt;
-    a.team_scratch = team_bytes;
-    launch(false);
+    launch();
     CUDA_TRY(cudaGetLastError());
   }
   return scratch_release(c, slot, st);

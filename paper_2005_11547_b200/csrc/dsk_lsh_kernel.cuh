@@ -31,19 +31,11 @@
 #ifndef DSK_LSH_FUSE
 #define DSK_LSH_FUSE 1  // dart-0 fusion for the LSH sink (1.8 % faster since the per-bucket slots)
 #endif
-// kCompact: a hit is stored as its fingerprint (fpa) and its rank rounded to
-// float (fra), 12 bytes instead of 16, so a launch's hit slots stay in L2; a
-// set whose selection needs the exact ranks (equal float keys among a
-// bucket's K + 1 smallest) or whose bucket outgrows its S slots is handed to
-// the exact retry launch (full {fp, rank bits} entries).
-template <bool kCompact>
 struct LshSink {
   static constexpr bool kFuse = DSK_LSH_FUSE != 0;
-  ulonglong2 *buf;      // exact: {fp, rank bits}, bucket b's first S hits at b*S
-  ulonglong2 *ovf;      // exact: hits beyond a bucket's S slots
-  uint32_t *ovf_b;      // exact: their buckets
-  uint64_t *fpa;        // compact: fingerprints, bucket b's at b*S
-  uint32_t *fra;        // compact: float(rank) bit patterns, bucket b's at b*S
+  ulonglong2 *buf;      // global: {fp, rank bits}, bucket b's first S hits at b*S
+  ulonglong2 *ovf;      // global: hits beyond a bucket's S slots
+  uint32_t *ovf_b;      // global: their buckets
   uint32_t S;           // slots per bucket
   uint32_t cap;         // overflow capacity
   ModU32 md;
@@ -72,15 +64,6 @@ struct LshSink {
       if (!(DSK_LSH_CLOSE && prev[bucket] >= K)) {
         const unsigned slot = atomicAdd(&cnt[bucket], 1u);
         if (slot == K - 1) atomicAdd(full, 1u);
-        if (kCompact) {
-          if (slot < S) {
-            fpa[(size_t)bucket * S + slot] = h.fp;
-            fra[(size_t)bucket * S + slot] = __float_as_uint(__double2float_rn(h.rank));
-          } else {
-            atomicOr(overflow, 1);  // the set goes to the exact retry launch
-          }
-          return;
-        }
         const ulonglong2 e =
             make_ulonglong2(h.fp, (unsigned long long)__double_as_longlong(h.rank));
         if (slot < S) {
@@ -141,11 +124,7 @@ __host__ __device__ inline size_t lsh_smem(int L, int G, int nw) {
 
 // kGC: the per-bucket counters live in the team's global scratch instead of
 // shared memory (L too large for shared memory; instantiated for NW = 20)
-__host__ __device__ inline size_t lsh_compact_scratch(int L, uint32_t S) {  // fra | fpa
-  return align128((size_t)L * S * 4) + align128((size_t)L * S * 8);
-}
-
-template <int NW, bool kGC = false, bool kCompact = false>
+template <int NW, bool kGC = false>
 __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
@@ -173,8 +152,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   // slots L*S*16 | overflow cap*16 | overflow buckets cap*4 | selection
   // L*K*8 | (kGC) counters
   const size_t o_ovf = align128((size_t)L * a.S * 16), o_ovb = o_ovf + align128((size_t)a.cap * 16);
-  const size_t o_sel = o_ovb + align128((size_t)a.cap * 4);
-  const size_t o_cnt = kCompact ? lsh_compact_scratch(L, a.S) : o_sel + align128((size_t)L * K * 8);
+  const size_t o_sel = o_ovb + align128((size_t)a.cap * 4), o_cnt = o_sel + align128((size_t)L * K * 8);
   unsigned char *cb = kGC ? gs + o_cnt : tb + kTeamCtlBytes;
   unsigned int *cnt = reinterpret_cast<unsigned int *>(cb);
   unsigned int *off = cnt + L;
@@ -186,15 +164,9 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   uint32_t *ovf_b = reinterpret_cast<uint32_t *>(gs + o_ovb);
   uint64_t *sel = reinterpret_cast<uint64_t *>(gs + o_sel);
   const uint32_t S = a.S;
-  // compact layout: float ranks L*S*4 | fingerprints L*S*8 (the K selected
-  // fingerprints of bucket b are written back over its own slots b*S..)
-  uint32_t *fra = reinterpret_cast<uint32_t *>(gs);
-  uint64_t *fpa = reinterpret_cast<uint64_t *>(gs + align128((size_t)L * S * 4));
   __syncthreads();
 
-  LshSink<kCompact> sink;
-  sink.fpa = fpa;
-  sink.fra = fra;
+  LshSink sink;
   sink.buf = buf;
   sink.ovf = ovf;
   sink.ovf_b = ovf_b;
@@ -286,7 +258,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           for (int i = tt; i < L; i += G * 32) off[i] = cnt[i];  // band snapshot
           team_sync(G, team);
           if (ab || areas > kMaxAreas) err = DSK_AREAS;  // ref/darthash.py:243
-          else if (ovf) err = kCompact ? DSK_RETRY : DSK_SCRATCH;
+          else if (ovf) err = DSK_SCRATCH;
           else if (a.force_retry && phi == phi0 && phi0 > 1) err = DSK_RETRY;  // tests
           if (!err) {
             final_areas = areas;
@@ -307,7 +279,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         if (err) {
           // a failing first band at phi0 > 1: the host's retry launch redoes
           // the set from phi = 1 (dsk_lsh_csr)
-          status = ((phi == phi0 && phi0 > 1) || err == DSK_RETRY) ? DSK_RETRY : err;
+          status = (phi == phi0 && phi0 > 1) ? DSK_RETRY : err;
           break;
         }
         L_prev = Lim;
@@ -317,104 +289,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
     unsigned wd = __reduce_add_sync(DSK_FULL, n_darts), wh = __reduce_add_sync(DSK_FULL, n_hits);
     if (lane == 0) { atomicAdd(&C.darts, wd); atomicAdd(&C.hits, wh); }
     team_sync(G, team);
-    if (kCompact && status == 0) {
-      // ---- compact selection (ref/annindex.py:77-81): the K smallest float
-      // keys of each bucket, in order.  Float rounding is monotone, so when
-      // no selected key has an equal twin the order and the K-set equal the
-      // exact (rank, fp) order; otherwise the set is handed to the exact
-      // retry launch.  <= 64 entries: 64-wide bitonic sort + a binary search
-      // per entry for its position; 65..128: counting; more: retry.
-      for (int b = wit; b < L; b += G) {
-        const unsigned nb = cnt[b] < S ? cnt[b] : S;
-        const uint32_t *frb = fra + (size_t)b * S;
-        uint64_t *fpb = fpa + (size_t)b * S;
-        uint32_t own[4];
-        unsigned pos[4];
-        bool coll = false;
-#pragma unroll
-        for (int h = 0; h < 4; h++) {
-          const unsigned i = lane + 32 * h;
-          own[h] = (h < 2 || nb > 64) && i < nb ? frb[i] : 0xffffffffu;
-          pos[h] = 0xffffffffu;
-        }
-        if (nb <= 64) {
-          uint32_t key[2] = {own[0], own[1]};
-          for (int kk = 2; kk <= 64; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-              if (j == 32) {
-                if (key[1] < key[0]) { uint32_t t0 = key[0]; key[0] = key[1]; key[1] = t0; }
-              } else {
-#pragma unroll
-                for (int h = 0; h < 2; h++) {
-                  int p = lane + 32 * h;
-                  uint32_t y = __shfl_xor_sync(DSK_FULL, key[h], j);
-                  bool take_min = ((p & j) == 0) == ((p & kk) == 0);
-                  if (take_min == (y < key[h])) key[h] = y;
-                }
-              }
-            }
-          }
-          uint32_t nx = __shfl_down_sync(DSK_FULL, key[0], 1);
-          const uint32_t f1 = __shfl_sync(DSK_FULL, key[1], 0);
-          if (lane == 31) nx = f1;
-          coll = (unsigned)lane < (unsigned)K && (unsigned)lane + 1 < nb && nx == key[0];
-#pragma unroll
-          for (int h = 0; h < 2; h++) {
-            unsigned q = 0;  // #{sorted first-32 keys < own}
-#pragma unroll
-            for (int step = 16; step >= 1; step >>= 1) {
-              uint32_t v = __shfl_sync(DSK_FULL, key[0], (int)q + step - 1);
-              if (v < own[h]) q += step;
-            }
-            pos[h] = q;
-          }
-        } else if (nb <= 128) {
-          unsigned lt[4] = {0, 0, 0, 0}, eq[4] = {0, 0, 0, 0};
-#pragma unroll
-          for (int c = 0; c < 4; c++) {
-            for (unsigned l = 0; l < 32 && 32 * c + l < nb; l++) {
-              const uint32_t kj = __shfl_sync(DSK_FULL, own[c], (int)l);
-#pragma unroll
-              for (int h = 0; h < 4; h++) {
-                lt[h] += kj < own[h];
-                eq[h] += kj == own[h];
-              }
-            }
-          }
-#pragma unroll
-          for (int h = 0; h < 4; h++) {
-            pos[h] = lt[h];
-            if (lane + 32u * h < nb && lt[h] < (unsigned)K && eq[h] > 1) coll = true;
-          }
-        } else {
-          coll = true;
-        }
-        if (__any_sync(DSK_FULL, coll)) {
-          if (lane == 0) atomicOr(&C.overflow, 1);
-        } else {
-          // the K selected fingerprints move to slots 0..K-1 of the bucket
-          uint64_t v[4];
-#pragma unroll
-          for (int h = 0; h < 4; h++) {
-            const unsigned i = lane + 32 * h;
-            v[h] = i < nb && pos[h] < (unsigned)K ? fpb[i] : 0;
-          }
-          __syncwarp();
-#pragma unroll
-          for (int h = 0; h < 4; h++) {
-            const unsigned i = lane + 32 * h;
-            if (i < nb && pos[h] < (unsigned)K) fpb[pos[h]] = v[h];
-          }
-        }
-#if DSK_LSH_DISCARD
-        for (unsigned q = lane; q < (nb * 4 + 127) / 128; q += 32) l2_discard(frb + 32 * q);
-#endif
-      }
-      __threadfence_block();
-      team_sync(G, team);
-      if (C.overflow) status = DSK_RETRY;
-    }
-    if (!kCompact && status == 0) {
+    if (status == 0) {
       // ---- selection (ref/annindex.py:77-81): bucket b's hits sit in its S
       // slots (plus, past S, in the overflow list)
       const unsigned ovf_n = C.total < a.cap ? C.total : a.cap;
@@ -619,10 +494,8 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       if (__any_sync(DSK_FULL, tie) && lane == 0) atomicOr(&C.tie, 1);
       __threadfence_block();
       team_sync(G, team);
-      // ---- epilogue (below): mix64 per table (ref/randomness.py:160-166):
+      // ---- epilogue: mix64 per table (ref/randomness.py:160-166):
       // mixed = hash64(element = v ^ mixed, w = position, stream 12)
-    }
-    if (status == 0) {
       const uint64_t mconst = T.tNu[0] ^ T.tRho[0] ^ __ldg(&a.tabs.tab[12 * 256]) ^
                               __ldg(&a.tabs.tab[13 * 256]) ^ T.tR[0][0] ^ T.tR[1][0] ^
                               __ldg(&a.tabs.tab[16 * 256]) ^ __ldg(&a.tabs.tab[17 * 256]) ^
@@ -630,10 +503,9 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
                               __ldg(&a.tabs.tab[20 * 256 + kStreamKeyMix]) ^
                               __ldg(&a.tabs.tab[21 * 256]);
       for (int b = tt; b < L; b += G * 32) {
-        const uint64_t *selb = kCompact ? fpa + (size_t)b * S : sel + (size_t)b * K;
         uint64_t mixed = 0;
         for (int p = 0; p < K; p++) {
-          uint64_t v = selb[p];
+          uint64_t v = sel[(size_t)b * K + p];
           if (a.out_fps) a.out_fps[((size_t)s * L + b) * K + p] = v;
           uint64_t e = v ^ mixed;
           uint64_t h = mconst ^ T.tW[0][p & 0xff] ^ T.tW[1][(p >> 8) & 0xff];
@@ -645,15 +517,8 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       }
 #if DSK_LSH_DISCARD
       team_sync(G, team);  // every table's selection has been read
-      if (kCompact) {
-        for (int b = tt; b < L; b += G * 32) {
-          const unsigned nb = cnt[b] < S ? cnt[b] : S;
-          for (unsigned q = 0; q < (nb * 8 + 127) / 128; q++) l2_discard(fpa + (size_t)b * S + 16 * q);
-        }
-      } else {
-        const unsigned sel_lines = ((unsigned)L * K * 8 + 127) / 128;
-        for (unsigned q = tt; q < sel_lines; q += G * 32) l2_discard(sel + 16 * q);
-      }
+      const unsigned sel_lines = ((unsigned)L * K * 8 + 127) / 128;
+      for (unsigned q = tt; q < sel_lines; q += G * 32) l2_discard(sel + 16 * q);
 #endif
     } else {
       for (int b = tt; b < L; b += G * 32) {

@@ -300,25 +300,3 @@ def test_l1_pairwise_all_small_and_deep_sizes():
     got = l1_batch(indptr, w).cpu().numpy()
     exp = np.array([float(np.sum(w[indptr[s]:indptr[s + 1]])) for s in range(lens.size)])
     assert np.array_equal(got, exp)
-
-
-@pytest.mark.gpu
-@pytest.mark.parametrize("compact", ["0", "1"])
-@pytest.mark.parametrize("slots", [None, "64"])
-def test_lsh_compact_and_exact_slots_agree(monkeypatch, compact, slots):
-    """Compact 12-byte hit slots (fingerprint + float rank, sets needing exact
-    ranks handed to the exact retry launch) and full 16-byte slots give the
-    oracle's keys; with 64 slots per bucket the compact launch hands the
-    overflowing sets back and the exact launch uses its overflow list."""
-    from paper_2005_11547_b200 import HashFamily, LshParams, as_u64, lsh_batch
-    monkeypatch.setenv("DSK_LSH_COMPACT", compact)
-    if slots:
-        monkeypatch.setenv("DSK_LSH_SLOTS", slots)
-    indptr, ids, w = workloads.generate("cfg4", n=500, start=123456)
-    res = lsh_batch(indptr, ids, w, LshParams(100, 20), HashFamily(3), fps=True)
-    keys, fps, status, phi, hits = Oracle(3).lsh_csr(indptr, ids, w, 100, 20, want_fps=True)
-    assert (status == 0).all() and (res.status.cpu().numpy() == 0).all()
-    assert np.array_equal(as_u64(res.keys), keys)
-    assert np.array_equal(as_u64(res.fps), fps)
-    assert np.array_equal(res.phi.cpu().numpy(), phi)
-    assert np.array_equal(res.stats.cpu().numpy()[:, 2], hits)
