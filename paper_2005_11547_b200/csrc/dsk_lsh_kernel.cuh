@@ -3,7 +3,7 @@
 #define DSK_LSH_CLOSE 1  // drop hits of buckets already full when the band began
 #endif
 #ifndef DSK_LSH_DISCARD
-#define DSK_LSH_DISCARD 1  // discard spent hit-slot / selection lines from L2 (no write-back)
+#define DSK_LSH_DISCARD 0  // 1: discard spent hit-slot / selection lines from L2 (no write-back; measured -40 % DRAM traffic, +2 % time)
 #endif
 #ifndef DSK_LSH_FAST
 #define DSK_LSH_FAST 1  // 0: exact sort only; 1: float-key sort + exact fallback; 2: timing only
