@@ -79,7 +79,7 @@ struct BottomKSink {
 
 __global__ void __launch_bounds__(kWarps * 32, 1) bottomk_kernel(BottomKArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
+  SmemTables &T = g_tabs;
   load_tables(T, a.tabs);
   const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);

@@ -135,6 +135,13 @@ struct TableArgs {
   double tf;
 };
 
+// The hash tables live in STATIC shared memory: their addresses are link-time
+// constants, so every table lookup is one LDS with an immediate offset (in
+// dynamic shared memory the compiler rematerialises the window base,
+// S2R + LEA, and adds it to every lookup address).  Dynamic shared memory
+// (warp queues, team blocks, slots) follows it.
+__shared__ __align__(16) SmemTables g_tabs;
+
 __device__ void load_tables(SmemTables &T, const TableArgs &a) {
   const int tid = threadIdx.x, nt = blockDim.x;
   for (int i = tid; i < 8 * 256; i += nt) (&T.tE[0][0])[i] = a.tab[i];
@@ -167,7 +174,7 @@ __device__ void load_tables(SmemTables &T, const TableArgs &a) {
 __host__ __device__ constexpr size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
 __host__ __device__ constexpr size_t align128(size_t x) { return (x + 127) & ~(size_t)127; }
 
-constexpr size_t kOffQueues = align16(sizeof(SmemTables));
+constexpr size_t kOffQueues = 0;  // dynamic shared memory begins with the warp queues (tables: g_tabs)
 constexpr size_t kQBytes = align16(sizeof(WarpQueues));
 constexpr size_t kOffTeam = kOffQueues + kWarps * kQBytes;
 // minhash / LSH kernels are instantiated for several CTA widths (warps per
@@ -397,7 +404,7 @@ __device__ __forceinline__ int opaque_team(int v) {
 template <int NW, bool kGlobal = false>
 __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
+  SmemTables &T = g_tabs;
   load_tables(T, a.tabs);
   const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
   const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
@@ -576,7 +583,7 @@ struct RowSink {
 
 __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
-  SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
+  SmemTables &T = g_tabs;
   load_tables(T, a.tabs);
   const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
@@ -844,6 +851,13 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
   CUDA_TRY(cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device));
   int smem_optin = 0;
   CUDA_TRY(cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device));
+  // the engine kernels hold the tables in static shared memory (g_tabs); the
+  // dynamic budget is the opt-in maximum minus that
+  {
+    cudaFuncAttributes fa;
+    CUDA_TRY(cudaFuncGetAttributes(&fa, lsh_kernel<24>));
+    smem_optin -= (int)fa.sharedSizeBytes;
+  }
   c->max_smem = (size_t)smem_optin;
   uint64_t pthr[64];
   for (int m = 0; m < 64; m++) {

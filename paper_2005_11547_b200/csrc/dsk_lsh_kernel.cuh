@@ -5,6 +5,13 @@
 #ifndef DSK_LSH_DISCARD
 #define DSK_LSH_DISCARD 0  // 1: discard spent hit-slot / selection lines from L2 (no write-back; measured -40 % DRAM traffic, +2 % time)
 #endif
+#ifndef DSK_LSH_SSEL
+#define DSK_LSH_SSEL 1  // selections staged in the team's idle warp queues (shared memory; 5 % faster on cfg4)
+#endif
+#ifndef DSK_LSH_PF
+#define DSK_LSH_PF 0  // 1: fetch the next bucket's hit slots into registers, 2/3: prefetch them to L2/L1
+                        // (measured: 1 +9.6 % time from engine spills, 2/3 +0.9 %)
+#endif
 #ifndef DSK_LSH_FAST
 #define DSK_LSH_FAST 1  // 0: exact sort only; 1: float-key sort + exact fallback; 2: timing only
 #endif
@@ -45,22 +52,15 @@ struct LshSink {
   const unsigned int *prev;  // cnt at the start of this band
   unsigned int *full;   // buckets holding >= K hits
   int *overflow;
-  // First band of a phi0 > 1 start: hits with rank <= L1 = fl(1 / l1) are
-  // also counted per bucket, cnt1 = prev + L, and buckets reaching K in
-  // full[1], to recover phi* = 1 and H(1).  L1 sits in the team block at
-  // full + 2 (< 0: no split in this band); nothing extra is held in registers.
 
   // Bands are rank-ordered, so a bucket that held >= K darts when this band
   // began can never take a dart of this band into its K smallest: those hits
   // are not buffered (they still count toward H(phi*) in the engine).
+  // (phi* = 1 inside a phi0 = 2 first band is recovered at selection time
+  // from each bucket's K-th smallest rank, so nothing else is counted here.)
   __device__ void hit(bool valid, const HitInfo &h, int lane) {
     if (valid) {
       const uint32_t bucket = mod_u32(h.bhash, md);
-      const double L1 = *reinterpret_cast<const double *>(full + 2);
-      if (L1 >= 0.0 && h.rank <= L1) {
-        if (atomicAdd(const_cast<unsigned int *>(prev) + md.d + bucket, 1u) == K - 1)
-          atomicAdd(full + 1, 1u);
-      }
       if (!(DSK_LSH_CLOSE && prev[bucket] >= K)) {
         const unsigned slot = atomicAdd(&cnt[bucket], 1u);
         if (slot == K - 1) atomicAdd(full, 1u);
@@ -122,242 +122,173 @@ __host__ __device__ inline size_t lsh_smem(int L, int G, int nw) {
   return off_team(nw) + (size_t)teams * lsh_team_bytes(L);
 }
 
-// kGC: the per-bucket counters live in the team's global scratch instead of
-// shared memory (L too large for shared memory; instantiated for NW = 20)
-template <int NW, bool kGC = false>
-__global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
-  extern __shared__ __align__(16) unsigned char smem[];
-  SmemTables &T = *reinterpret_cast<SmemTables *>(smem);
-  load_tables(T, a.tabs);
-  const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
-  const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
-            tt = opaque_team(wit * 32 + lane);
-  const int L = a.L, K = a.K;
-  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
-  const size_t tbytes = kGC ? kTeamCtlBytes : lsh_team_bytes(L);
-#if DSK_OPAQUE_TB
-  unsigned char *tb = smem + opaque_int((int)(off_team(NW) + team * tbytes));
-#else
-  unsigned char *tb = smem + off_team(NW) + team * tbytes;
-#endif
-  TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
-  // global scratch of this team
-  const int teams = NW / G;
-#if DSK_OPAQUE_TB
-  unsigned char *gs = a.scratch + opaque_size(((size_t)blockIdx.x * teams + team) * a.team_scratch);
-#else
-  unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
-#endif
-  // team scratch (128-byte aligned regions, so spent lines can be discarded):
-  // slots L*S*16 | overflow cap*16 | overflow buckets cap*4 | selection
-  // L*K*8 | (kGC) counters
-  const size_t o_ovf = align128((size_t)L * a.S * 16), o_ovb = o_ovf + align128((size_t)a.cap * 16);
-  const size_t o_sel = o_ovb + align128((size_t)a.cap * 4), o_cnt = o_sel + align128((size_t)L * K * 8);
-  unsigned char *cb = kGC ? gs + o_cnt : tb + kTeamCtlBytes;
-  unsigned int *cnt = reinterpret_cast<unsigned int *>(cb);
-  unsigned int *off = cnt + L;
-  unsigned int *cnt1 = off + L;  // hits with rank <= fl(1 / l1), first band of a phi0 = 2 start
-  unsigned int *fullc =
-      reinterpret_cast<unsigned int *>(cb + align16((size_t)3 * L * sizeof(unsigned)));
-  ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
-  ulonglong2 *ovf = reinterpret_cast<ulonglong2 *>(gs + o_ovf);
-  uint32_t *ovf_b = reinterpret_cast<uint32_t *>(gs + o_ovb);
-  uint64_t *sel = reinterpret_cast<uint64_t *>(gs + o_sel);
-  const uint32_t S = a.S;
-  __syncthreads();
+// Selection + epilogue of one set (ref/annindex.py:77-81, :135), kept out
+// of line so its registers do not perturb the allocation of the enumeration
+// engine (the kernel runs at the 80-register limit).
+struct LshSel {
+  const SmemTables *T;
+  unsigned char *smem;
+  TeamCtl *C;
+  const unsigned *cnt;
+  unsigned *fullc;
+  const ulonglong2 *buf, *ovf;
+  const uint32_t *ovf_b;
+  uint64_t *sel;
+  const uint64_t *gtab;
+  uint64_t *out_fps, *out_keys;
+  long long s;
+  double Lsel;
+  int L, K, G, team, wit, lane, tt, exact_sort, phi0, phi_star;
+  uint32_t S, cap;
+};
 
-  LshSink sink;
-  sink.buf = buf;
-  sink.ovf = ovf;
-  sink.ovf_b = ovf_b;
-  sink.S = S;
-  sink.cap = a.cap;
-  sink.md = a.md;
-  sink.K = (uint32_t)K;
-  sink.total = &C.total;
-  sink.cnt = cnt;
-  sink.prev = off;  // band-start snapshot of cnt
-  sink.full = fullc;
-  sink.overflow = &C.overflow;
-
-  for (;;) {
-    if (tt == 0) {
-      long long q = (long long)atomicAdd(a.counter, 1ULL);
-      if (a.retry_rows)  // retry launch: the rows the first launch handed back
-        q = q < (long long)*a.retry_n ? (long long)a.retry_rows[q] : a.n;
-      C.set = q;
-    }
-    team_sync(G, team);
-    const long long s = C.set;
-    if (s >= a.n) break;
-    const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
-    for (int i = tt; i < L; i += G * 32) cnt[i] = off[i] = cnt1[i] = 0;
-    if (tt == 0) {
-      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0;
-      C.areas[0] = C.areas[1] = 0.0; C.chunk[0] = C.chunk[1] = 0;
-      C.darts = 0; C.hits = 0; C.total = 0; C.sexp = 0; C.overflow = 0;
-      fullc[0] = fullc[1] = 0;
-    }
-    team_sync(G, team);
-    if (wit == 0)
-      set_prologue(a.w, a.tf, T, C, lo, nnz, reinterpret_cast<double *>(&Q), lane,
-                   a.normalize != 0);
-    team_sync(G, team);
-    int status = C.status;
-    int phi_star = 0;
-    double final_areas = 0.0;
-    uint32_t n_darts = 0, n_hits = 0;
-    if (status == 0) {
-      const double l1 = C.l1;
-      const int maxd = C.maxdepth;
-      const int sexp = C.sexp;
-      // The first band is (0, phi0 / l1]: the keys do not depend on the phi
-      // schedule, and counting the hits with
-      // rank <= fl(1 / l1) per bucket recovers phi* = 1.  A first band that
-      // fails (limit, depth or area cap at phi0 that phi = 1 might not hit)
-      // is redone from phi = 1 by a second launch, stepping exactly as the
-      // reference does.
-      const int phi0 = a.phi0;
-      status = DSK_NOCONV;
-      double L_prev = -1.0;
-      int RD_prev = 0;
-      for (int phi = phi0; phi <= 64; phi++) {  // ref/annindex.py:70
-        int err = 0;
-        double Lim = __ddiv_rn((double)phi, l1);
-        int RD = 0;
-        if (!(Lim > 0.0) || isinf(Lim)) {
-          err = DSK_LIMIT;
-        } else {
-          RD = floor_log2_host(__dadd_rn(1.0, Lim), T.l2thr);
-          err = depth_status(maxd, RD);
-        }
-        if (!err) {
-          PassParams P;
-          P.gtab = a.tabs.tab;
-          P.inv_t = a.inv_t;
-          P.tf = a.tf;
-          P.L_hi = Lim;
-          P.L_lo = L_prev;
-          P.RD = RD;
-          P.RD_lo = RD_prev;
-          P.maxd = maxd;
-          poisson_regs(P, T);
-          const int par = phi & 1;
-          if (tt == 0)
-            *reinterpret_cast<double *>(fullc + 2) =
-                (phi == phi0 && phi0 > 1) ? __ddiv_rn(1.0, l1) : -1.0;
-          team_sync(G, team);
-          run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
-                   par, sexp);
-          team_sync(G, team);
-          const double areas = C.areas[par];
-          const bool ab = C.abort != 0;
-          const unsigned full = fullc[0], full1 = fullc[1];
-          const bool ovf = C.overflow != 0;
-          if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
-          for (int i = tt; i < L; i += G * 32) off[i] = cnt[i];  // band snapshot
-          team_sync(G, team);
-          if (ab || areas > kMaxAreas) err = DSK_AREAS;  // ref/darthash.py:243
-          else if (ovf) err = DSK_SCRATCH;
-          else if (a.force_retry && phi == phi0 && phi0 > 1) err = DSK_RETRY;  // tests
-          if (!err) {
-            final_areas = areas;
-            // ref/annindex.py:72-76: >= L*K darts and every bucket >= K
-            if (full == (unsigned)L) {  // implies >= L*K darts
-              status = DSK_OK;
-              phi_star = phi;
-              if (phi == phi0 && phi0 > 1 && full1 == (unsigned)L) {
-                phi_star = 1;  // H(1) = the hits counted below fl(1 / l1)
-                n_hits = 0;
-                if (wit == 0)
-                  for (int i = lane; i < L; i += 32) n_hits += cnt1[i];
-              }
-              break;
-            }
-          }
-        }
-        if (err) {
-          // a failing first band at phi0 > 1: the host's retry launch redoes
-          // the set from phi = 1 (dsk_lsh_csr)
-          status = (phi == phi0 && phi0 > 1) ? DSK_RETRY : err;
-          break;
-        }
-        L_prev = Lim;
-        RD_prev = RD;
+#ifndef DSK_LSH_SEL_NOINLINE
+#define DSK_LSH_SEL_NOINLINE 0
+#endif
+#if DSK_LSH_SEL_NOINLINE
+__device__ __noinline__
+#else
+__device__ __forceinline__
+#endif
+int lsh_select(const LshSel &x) {
+  const SmemTables &T = *x.T;
+  unsigned char *smem = x.smem;
+  TeamCtl &C = *x.C;
+  const unsigned *cnt = x.cnt;
+  unsigned *fullc = x.fullc;
+  const ulonglong2 *buf = x.buf, *ovf = x.ovf;
+  const uint32_t *ovf_b = x.ovf_b;
+  uint64_t *sel = x.sel;
+  const long long s = x.s;
+  const double Lsel = x.Lsel;
+  const int L = x.L, K = x.K, G = x.G, team = x.team, wit = x.wit, lane = x.lane, tt = x.tt;
+  const uint32_t S = x.S;
+  int phi_star = x.phi_star;
+    // ---- selection (ref/annindex.py:77-81): bucket b's hits sit in its S
+    // slots (plus, past S, in the overflow list).  K smallest of each
+    // bucket by (rank bits, fp); bit-identical ranks with different
+    // fingerprints flag a tie (the reference orders them by index tuple).
+    //
+    // Buckets of <= 64 entries (nearly all: ~40 per bucket at cfg4's
+    // stopping step) are sorted in registers.  With K <= 32 the sort key is
+    // 32 bits: a 26-bit fixed-point rank q = floor(rank * 2^26 / limit)
+    // (monotone in the rank, every buffered rank is <= the final limit)
+    // above the entry's 6-bit index, so the sorted position names its entry
+    // directly; when two of the first K + 1 sorted keys share q the bucket
+    // is redone on the exact (rank bits, fp) pair.  Larger buckets rank
+    // each entry by counting.  (Fetching the next bucket's entries ahead,
+    // DSK_LSH_PF, costs more in engine register spills than it hides.)
+    //
+    // phi* = 1 inside a phi0 = 2 first band: bucket b held >= K hits with
+    // rank <= L1 = fl(1 / l1) iff its K-th smallest rank is <= L1; when all
+    // L buckets do, phi* = 1 (the K smallest are the same darts) and H(1)
+    // is recounted from the buffer.
+    const unsigned ovf_n = C.total < x.cap ? C.total : x.cap;
+    const bool chk1 = phi_star == x.phi0 && x.phi0 > 1;
+    const double L1 = chk1 ? __ddiv_rn(1.0, C.l1) : -1.0;
+    const double qscale = __ddiv_rn(67108864.0, Lsel);  // 2^26 / limit
+    const bool fastK = K <= 32 && DSK_LSH_FAST != 0 && !x.exact_sort && qscale < 1e300;
+    const bool fast64 = DSK_LSH_FAST != 0 && !x.exact_sort;
+    unsigned *full1 = fullc + 1;
+    // selections of up to TB tables at a time in the team's (now idle) warp
+    // queues, row stride K | 1 words (conflict-free column reads in the
+    // epilogue); the global `sel` when one table does not fit
+    const int KS = K | 1;
+    const int cap_s = (int)((size_t)G * kQBytes / 8);
+    const bool in_smem = DSK_LSH_SSEL && cap_s >= KS;
+    // (a multiple of the team's thread count, so no epilogue round is partial)
+    const int TB = in_smem ? (cap_s / KS >= G * 32 ? cap_s / KS / (G * 32) * (G * 32) : cap_s / KS) : L;
+    const int rs = in_smem ? KS : K;
+    uint64_t *sq = reinterpret_cast<uint64_t *>(smem + kOffQueues + (size_t)team * G * kQBytes);
+    bool tie = false;
+    auto fetch = [&](int b, ulonglong2 (&e)[2]) {
+      const unsigned nb = cnt[b];
+      const ulonglong2 *src = buf + (size_t)b * S;
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const unsigned i = lane + 32 * h;
+        e[h] = (nb <= 64 && i < nb) ? src[i] : make_ulonglong2(~0ULL, ~0ULL);
       }
-    }
-    unsigned wd = __reduce_add_sync(DSK_FULL, n_darts), wh = __reduce_add_sync(DSK_FULL, n_hits);
-    if (lane == 0) { atomicAdd(&C.darts, wd); atomicAdd(&C.hits, wh); }
-    team_sync(G, team);
-    if (status == 0) {
-      // ---- selection (ref/annindex.py:77-81): bucket b's hits sit in its S
-      // slots (plus, past S, in the overflow list)
-      const unsigned ovf_n = C.total < a.cap ? C.total : a.cap;
-      // K smallest of each bucket by (rank bits, fp).  Buckets of <= 64
-      // entries (nearly all: ~40 per bucket at cfg4's stopping step) are
-      // sorted in registers with a 64-wide bitonic network, first on a packed
-      // {float rank, buffer index} key and, if two of the first K + 1 float
-      // ranks coincide, again on the exact (rank bits, fp) pair; larger
-      // buckets rank each entry by counting.  Bit-identical ranks with
-      // different fingerprints flag a tie (the reference orders them by
-      // index tuple).
-      bool tie = false;
-      for (int b = wit; b < L; b += G) {
+    };
+    for (int c0 = 0; c0 < L; c0 += TB) {
+      const int c1 = c0 + TB < L ? c0 + TB : L;
+      uint64_t *selp = in_smem ? sq : sel + (size_t)c0 * K;
+      ulonglong2 e[2], en[2];
+      if (fastK && c0 + wit < c1) fetch(c0 + wit, e);
+      for (int b = c0 + wit; b < c1; b += G) {
         const unsigned nb = cnt[b];
         const size_t o = (size_t)b * S;  // bucket b's slots (nb <= 64 <= S on the register paths)
-        bool exact = nb > 64 || DSK_LSH_FAST == 0 || a.exact_sort;
-        if (!exact && K <= 32) {
-          // fast path: bitonic sort of the 32-bit float-rounded ranks (float
-          // rounding is monotone); when the first K + 1 sorted keys are
-          // distinct, their order and the K-set equal the exact (rank, fp)
-          // order, and each entry finds its own position by a 5-step binary
-          // search over the sorted first 32 keys.  Otherwise the bucket takes
-          // the exact path below.
-          uint32_t key[2], own[2];
+        uint64_t *row = selp + (size_t)(b - c0) * rs;
+        if (fastK && b + G < c1) { if (DSK_LSH_PF == 1) fetch(b + G, en); }
+        if (DSK_LSH_PF >= 2 && b + G < c1) {
+          // prefetch the next bucket's slot lines (no registers held)
+          const unsigned nn = cnt[b + G];
+          const unsigned lines = ((nn < 64 ? nn : 64) * 16 + 127) / 128;
+          if ((unsigned)lane < lines) {
+            const ulonglong2 *pa = buf + (size_t)(b + G) * S + 8 * lane;
+            if (DSK_LSH_PF == 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
+            else asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
+          }
+        }
+        if (DSK_LSH_PF != 1 && fastK && b != c0 + wit) fetch(b, e);
+        bool exact = nb > 64 || !fast64;
+        if (!exact && fastK) {
+          uint32_t key[2];
 #pragma unroll
           for (int h = 0; h < 2; h++) {
-            unsigned i = lane + 32 * h;
-            own[h] = i < nb ? __float_as_uint(__double2float_rn(
-                                  __longlong_as_double((long long)buf[o + i].y)))
-                            : 0xffffffffu;  // above every float bit pattern of a rank
-            key[h] = own[h];
+            const unsigned i = lane + 32 * h;
+            double qd = __dmul_rn(__longlong_as_double((long long)e[h].y), qscale);
+            uint32_t q = qd < 67108863.0 ? (uint32_t)qd : 67108863u;
+            key[h] = i < nb ? (q << 6) | i : 0xffffffffu;
           }
-          for (int kk = 2; kk <= 64; kk <<= 1) {
-            for (int j = kk >> 1; j > 0; j >>= 1) {
-              if (j == 32) {
-                if (key[1] < key[0]) { uint32_t t0 = key[0]; key[0] = key[1]; key[1] = t0; }
-              } else {
+          if (nb <= 32) {
+            for (int kk = 2; kk <= 32; kk <<= 1) {
+              for (int j = kk >> 1; j > 0; j >>= 1) {
+                uint32_t y = __shfl_xor_sync(DSK_FULL, key[0], j);
+                bool take_min = ((lane & j) == 0) == ((lane & kk) == 0);
+                if (take_min == (y < key[0])) key[0] = y;
+              }
+            }
+          } else {
+            for (int kk = 2; kk <= 64; kk <<= 1) {
+              for (int j = kk >> 1; j > 0; j >>= 1) {
+                if (j == 32) {
+                  if (key[1] < key[0]) { uint32_t t0 = key[0]; key[0] = key[1]; key[1] = t0; }
+                } else {
 #pragma unroll
-                for (int h = 0; h < 2; h++) {
-                  int p = lane + 32 * h;
-                  uint32_t y = __shfl_xor_sync(DSK_FULL, key[h], j);
-                  bool take_min = ((p & j) == 0) == ((p & kk) == 0);
-                  if (take_min == (y < key[h])) key[h] = y;
+                  for (int h = 0; h < 2; h++) {
+                    int p = lane + 32 * h;
+                    uint32_t y = __shfl_xor_sync(DSK_FULL, key[h], j);
+                    bool take_min = ((p & j) == 0) == ((p & kk) == 0);
+                    if (take_min == (y < key[h])) key[h] = y;
+                  }
                 }
               }
             }
           }
-          // positions 0..K (K <= 32: lanes 0..K of key[0], position 32 = lane 0 of key[1])
+          // positions 0..K (K <= 32): lane p holds position p, position 32
+          // is lane 0 of key[1]; equal q among them -> exact path
           uint32_t nx = __shfl_down_sync(DSK_FULL, key[0], 1);
           uint32_t f1 = __shfl_sync(DSK_FULL, key[1], 0);
           if (lane == 31) nx = f1;
-          const bool coll = (unsigned)lane < (unsigned)K && (unsigned)lane + 1 < nb && nx == key[0];
-          exact = __any_sync(DSK_FULL, coll) && DSK_LSH_FAST == 1;
+          const bool coll = (unsigned)lane < (unsigned)K && (unsigned)lane + 1 < nb &&
+                            (nx >> 6) == (key[0] >> 6);
+          exact = __any_sync(DSK_FULL, coll);
           if (!exact) {
-#pragma unroll
-            for (int h = 0; h < 2; h++) {
-              unsigned pos = 0;  // #{sorted first-32 keys < own}
-#pragma unroll
-              for (int step = 16; step >= 1; step >>= 1) {
-                uint32_t v = __shfl_sync(DSK_FULL, key[0], (int)pos + step - 1);
-                if (v < own[h]) pos += step;
-              }
-              unsigned i = lane + 32 * h;
-              if (i < nb && pos < (unsigned)K) sel[(size_t)b * K + pos] = buf[o + i].x;
+            const uint32_t idx = key[0] & 63u;
+            const int srcl = (int)(idx & 31u);
+            const uint64_t fa = __shfl_sync(DSK_FULL, e[0].x, srcl);
+            const uint64_t fb = __shfl_sync(DSK_FULL, e[1].x, srcl);
+            if (lane < K) row[lane] = idx >= 32 ? fb : fa;
+            if (chk1) {
+              const uint64_t ra = __shfl_sync(DSK_FULL, e[0].y, srcl);
+              const uint64_t rb = __shfl_sync(DSK_FULL, e[1].y, srcl);
+              const double rk = __longlong_as_double((long long)(idx >= 32 ? rb : ra));
+              if (lane == K - 1 && rk <= L1) atomicAdd(full1, 1u);
             }
           }
         } else if (!exact) {
-          // fast path: bitonic sort of one 64-bit key per entry, the rank
+          // K > 32: bitonic sort of one 64-bit key per entry, the rank
           // rounded to float (monotone) above the entry's buffer index; when
           // the first K + 1 sorted keys have distinct float ranks their order
           // and the K-set equal the exact (rank, fp) order, else the bucket
@@ -399,12 +330,18 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
             unsigned p = lane + 32 * h;
             if (p < (unsigned)K && p + 1 < nb && (nx[h] >> 32) == (key[h] >> 32)) coll = true;
           }
-          exact = __any_sync(DSK_FULL, coll) && DSK_LSH_FAST == 1;
+          exact = __any_sync(DSK_FULL, coll);
           if (!exact) {
 #pragma unroll
             for (int h = 0; h < 2; h++) {
               unsigned p = lane + 32 * h;
-              if (p < (unsigned)K && p < nb) sel[(size_t)b * K + p] = buf[(uint32_t)key[h]].x;
+              if (p < (unsigned)K && p < nb) {
+                const ulonglong2 ent = buf[(uint32_t)key[h]];
+                row[p] = ent.x;
+                if (chk1 && p == (unsigned)K - 1 &&
+                    __longlong_as_double((long long)ent.y) <= L1)
+                  atomicAdd(full1, 1u);
+              }
             }
           }
         }
@@ -414,9 +351,9 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           for (int h = 0; h < 2; h++) {
             unsigned i = lane + 32 * h;
             if (i < nb) {
-              ulonglong2 e = buf[o + i];
-              kr[h] = e.y;
-              kf[h] = e.x;
+              ulonglong2 ent = buf[o + i];
+              kr[h] = ent.y;
+              kf[h] = ent.x;
             } else {
               kr[h] = ~0ULL;
               kf[h] = ~0ULL;
@@ -456,7 +393,9 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           for (int h = 0; h < 2; h++) {
             unsigned p = lane + 32 * h;
             if (p + 1 < nb && nxr[h] == kr[h] && nxf[h] != kf[h]) tie = true;
-            if (p < (unsigned)K) sel[(size_t)b * K + p] = kf[h];
+            if (p < (unsigned)K) row[p] = kf[h];
+            if (chk1 && p == (unsigned)K - 1 && __longlong_as_double((long long)kr[h]) <= L1)
+              atomicAdd(full1, 1u);
           }
         } else if (exact) {
           // > 64 entries: rank every entry by counting; entry m of the bucket
@@ -472,16 +411,18 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           };
           for (unsigned i = lane; i < nb; i += 32) {
             uint32_t ei;
-            ulonglong2 e = entry(i, ei);
+            ulonglong2 en2 = entry(i, ei);
             unsigned pos = 0;
             for (unsigned m = 0; m < nb; m++) {
               uint32_t mi;
               ulonglong2 f = entry(m, mi);
-              bool less = f.y < e.y || (f.y == e.y && (f.x < e.x || (f.x == e.x && mi < ei)));
+              bool less = f.y < en2.y || (f.y == en2.y && (f.x < en2.x || (f.x == en2.x && mi < ei)));
               pos += less;
-              if (f.y == e.y && mi != ei && f.x != e.x) tie = true;
+              if (f.y == en2.y && mi != ei && f.x != en2.x) tie = true;
             }
-            if (pos < (unsigned)K) sel[(size_t)b * K + pos] = e.x;
+            if (pos < (unsigned)K) row[pos] = en2.x;
+            if (chk1 && pos == (unsigned)K - 1 && __longlong_as_double((long long)en2.y) <= L1)
+              atomicAdd(full1, 1u);
           }
         }
         // the bucket's slots are spent: drop their L2 lines without a write-back
@@ -490,36 +431,232 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         const unsigned lines = ((nb < S ? nb : S) * 16 + 127) / 128;
         for (unsigned q = lane; q < lines; q += 32) l2_discard(buf + o + 8 * q);
 #endif
+        if (DSK_LSH_PF == 1 && fastK) { e[0] = en[0]; e[1] = en[1]; }
       }
-      if (__any_sync(DSK_FULL, tie) && lane == 0) atomicOr(&C.tie, 1);
       __threadfence_block();
       team_sync(G, team);
       // ---- epilogue: mix64 per table (ref/randomness.py:160-166):
       // mixed = hash64(element = v ^ mixed, w = position, stream 12)
-      const uint64_t mconst = T.tNu[0] ^ T.tRho[0] ^ __ldg(&a.tabs.tab[12 * 256]) ^
-                              __ldg(&a.tabs.tab[13 * 256]) ^ T.tR[0][0] ^ T.tR[1][0] ^
-                              __ldg(&a.tabs.tab[16 * 256]) ^ __ldg(&a.tabs.tab[17 * 256]) ^
-                              __ldg(&a.tabs.tab[18 * 256]) ^ __ldg(&a.tabs.tab[19 * 256]) ^
-                              __ldg(&a.tabs.tab[20 * 256 + kStreamKeyMix]) ^
-                              __ldg(&a.tabs.tab[21 * 256]);
-      for (int b = tt; b < L; b += G * 32) {
+      const uint64_t mconst = T.tNu[0] ^ T.tRho[0] ^ __ldg(&x.gtab[12 * 256]) ^
+                              __ldg(&x.gtab[13 * 256]) ^ T.tR[0][0] ^ T.tR[1][0] ^
+                              __ldg(&x.gtab[16 * 256]) ^ __ldg(&x.gtab[17 * 256]) ^
+                              __ldg(&x.gtab[18 * 256]) ^ __ldg(&x.gtab[19 * 256]) ^
+                              __ldg(&x.gtab[20 * 256 + kStreamKeyMix]) ^
+                              __ldg(&x.gtab[21 * 256]);
+      for (int b = c0 + tt; b < c1; b += G * 32) {
+        const uint64_t *row = selp + (size_t)(b - c0) * rs;
         uint64_t mixed = 0;
         for (int p = 0; p < K; p++) {
-          uint64_t v = sel[(size_t)b * K + p];
-          if (a.out_fps) a.out_fps[((size_t)s * L + b) * K + p] = v;
-          uint64_t e = v ^ mixed;
+          uint64_t v = row[p];
+          if (x.out_fps) x.out_fps[((size_t)s * L + b) * K + p] = v;
+          uint64_t e2 = v ^ mixed;
           uint64_t h = mconst ^ T.tW[0][p & 0xff] ^ T.tW[1][(p >> 8) & 0xff];
 #pragma unroll
-          for (int q = 0; q < 8; q++) h ^= T.tE[q][(e >> (8 * q)) & 0xff];
+          for (int q = 0; q < 8; q++) h ^= T.tE[q][(e2 >> (8 * q)) & 0xff];
           mixed = finalize(h);
         }
-        if (a.out_keys) a.out_keys[(size_t)s * L + b] = mixed;
+        if (x.out_keys) x.out_keys[(size_t)s * L + b] = mixed;
       }
 #if DSK_LSH_DISCARD
-      team_sync(G, team);  // every table's selection has been read
-      const unsigned sel_lines = ((unsigned)L * K * 8 + 127) / 128;
-      for (unsigned q = tt; q < sel_lines; q += G * 32) l2_discard(sel + 16 * q);
+      if (!in_smem) {
+        team_sync(G, team);  // every table's selection has been read
+        const unsigned sel_lines = ((unsigned)(c1 - c0) * K * 8 + 127) / 128;
+        for (unsigned q = tt; q < sel_lines; q += G * 32) l2_discard(selp + 16 * q);
+      }
 #endif
+      team_sync(G, team);  // the next chunk overwrites the selections
+    }
+    if (__any_sync(DSK_FULL, tie) && lane == 0) atomicOr(&C.tie, 1);
+    if (chk1) {
+      team_sync(G, team);
+      if (fullc[1] == (unsigned)L) {
+        // phi* = 1: H(1) = the buffered hits with rank <= L1 (every hit of
+        // the first band is buffered: no bucket was closed before it)
+        phi_star = 1;
+        unsigned c = 0;
+        for (int b = wit; b < L; b += G) {
+          const unsigned nb = cnt[b], ns = nb < S ? nb : S;
+          for (unsigned i = lane; i < ns; i += 32)
+            c += __longlong_as_double((long long)buf[(size_t)b * S + i].y) <= L1;
+        }
+        for (unsigned q = tt; q < ovf_n; q += G * 32)
+          c += __longlong_as_double((long long)ovf[q].y) <= L1;
+        c = __reduce_add_sync(DSK_FULL, c);
+        team_sync(G, team);
+        if (tt == 0) C.hits = 0;
+        team_sync(G, team);
+        if (lane == 0) atomicAdd(&C.hits, c);
+      }
+    }
+  return phi_star;
+}
+
+// kGC: the per-bucket counters live in the team's global scratch instead of
+// shared memory (L too large for shared memory; instantiated for NW = 20)
+template <int NW, bool kGC = false>
+__global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  SmemTables &T = g_tabs;
+  load_tables(T, a.tabs);
+  const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
+  const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
+            tt = opaque_team(wit * 32 + lane);
+  const int L = a.L, K = a.K;
+  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
+  const size_t tbytes = kGC ? kTeamCtlBytes : lsh_team_bytes(L);
+#if DSK_OPAQUE_TB
+  unsigned char *tb = smem + opaque_int((int)(off_team(NW) + team * tbytes));
+#else
+  unsigned char *tb = smem + off_team(NW) + team * tbytes;
+#endif
+  TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
+  // global scratch of this team
+  const int teams = NW / G;
+#if DSK_OPAQUE_TB
+  unsigned char *gs = a.scratch + opaque_size(((size_t)blockIdx.x * teams + team) * a.team_scratch);
+#else
+  unsigned char *gs = a.scratch + ((size_t)blockIdx.x * teams + team) * a.team_scratch;
+#endif
+  // team scratch (128-byte aligned regions, so spent lines can be discarded):
+  // slots L*S*16 | overflow cap*16 | overflow buckets cap*4 | selection
+  // L*K*8 | (kGC) counters
+  const size_t o_ovf = align128((size_t)L * a.S * 16), o_ovb = o_ovf + align128((size_t)a.cap * 16);
+  const size_t o_sel = o_ovb + align128((size_t)a.cap * 4), o_cnt = o_sel + align128((size_t)L * K * 8);
+  unsigned char *cb = kGC ? gs + o_cnt : tb + kTeamCtlBytes;
+  unsigned int *cnt = reinterpret_cast<unsigned int *>(cb);
+  unsigned int *off = cnt + L;
+  unsigned int *fullc =
+      reinterpret_cast<unsigned int *>(cb + align16((size_t)3 * L * sizeof(unsigned)));
+  ulonglong2 *buf = reinterpret_cast<ulonglong2 *>(gs);
+  ulonglong2 *ovf = reinterpret_cast<ulonglong2 *>(gs + o_ovf);
+  uint32_t *ovf_b = reinterpret_cast<uint32_t *>(gs + o_ovb);
+  uint64_t *sel = reinterpret_cast<uint64_t *>(gs + o_sel);
+  const uint32_t S = a.S;
+  __syncthreads();
+
+  LshSink sink;
+  sink.buf = buf;
+  sink.ovf = ovf;
+  sink.ovf_b = ovf_b;
+  sink.S = S;
+  sink.cap = a.cap;
+  sink.md = a.md;
+  sink.K = (uint32_t)K;
+  sink.total = &C.total;
+  sink.cnt = cnt;
+  sink.prev = off;  // band-start snapshot of cnt
+  sink.full = fullc;
+  sink.overflow = &C.overflow;
+
+  for (;;) {
+    if (tt == 0) {
+      long long q = (long long)atomicAdd(a.counter, 1ULL);
+      if (a.retry_rows)  // retry launch: the rows the first launch handed back
+        q = q < (long long)*a.retry_n ? (long long)a.retry_rows[q] : a.n;
+      C.set = q;
+    }
+    team_sync(G, team);
+    const long long s = C.set;
+    if (s >= a.n) break;
+    const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
+    for (int i = tt; i < L; i += G * 32) cnt[i] = off[i] = 0;
+    if (tt == 0) {
+      C.filled = 0; C.tie = 0; C.abort = 0; C.status = 0;
+      C.areas[0] = C.areas[1] = 0.0; C.chunk[0] = C.chunk[1] = 0;
+      C.darts = 0; C.hits = 0; C.total = 0; C.sexp = 0; C.overflow = 0;
+      fullc[0] = fullc[1] = 0;
+    }
+    team_sync(G, team);
+    if (wit == 0)
+      set_prologue(a.w, a.tf, T, C, lo, nnz, reinterpret_cast<double *>(&Q), lane,
+                   a.normalize != 0);
+    team_sync(G, team);
+    int status = C.status;
+    int phi_star = 0;
+    double final_areas = 0.0, Lsel = 0.0;
+    uint32_t n_darts = 0, n_hits = 0;
+    if (status == 0) {
+      const double l1 = C.l1;
+      const int maxd = C.maxdepth;
+      const int sexp = C.sexp;
+      // The first band is (0, phi0 / l1]: the keys do not depend on the phi
+      // schedule, and phi* = 1 is recovered at
+      // selection time (every bucket's K-th smallest rank <= fl(1 / l1)).  A first band that
+      // fails (limit, depth or area cap at phi0 that phi = 1 might not hit)
+      // is redone from phi = 1 by a second launch, stepping exactly as the
+      // reference does.
+      const int phi0 = a.phi0;
+      status = DSK_NOCONV;
+      double L_prev = -1.0;
+      int RD_prev = 0;
+      for (int phi = phi0; phi <= 64; phi++) {  // ref/annindex.py:70
+        int err = 0;
+        double Lim = __ddiv_rn((double)phi, l1);
+        int RD = 0;
+        if (!(Lim > 0.0) || isinf(Lim)) {
+          err = DSK_LIMIT;
+        } else {
+          RD = floor_log2_host(__dadd_rn(1.0, Lim), T.l2thr);
+          err = depth_status(maxd, RD);
+        }
+        if (!err) {
+          PassParams P;
+          P.gtab = a.tabs.tab;
+          P.inv_t = a.inv_t;
+          P.tf = a.tf;
+          P.L_hi = Lim;
+          P.L_lo = L_prev;
+          P.RD = RD;
+          P.RD_lo = RD_prev;
+          P.maxd = maxd;
+          poisson_regs(P, T);
+          const int par = phi & 1;
+          team_sync(G, team);
+          run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
+                   par, sexp);
+          team_sync(G, team);
+          const double areas = C.areas[par];
+          const bool ab = C.abort != 0;
+          const unsigned full = fullc[0];
+          const bool ovf = C.overflow != 0;
+          if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
+          for (int i = tt; i < L; i += G * 32) off[i] = cnt[i];  // band snapshot
+          team_sync(G, team);
+          if (ab || areas > kMaxAreas) err = DSK_AREAS;  // ref/darthash.py:243
+          else if (ovf) err = DSK_SCRATCH;
+          else if (a.force_retry && phi == phi0 && phi0 > 1) err = DSK_RETRY;  // tests
+          if (!err) {
+            final_areas = areas;
+            // ref/annindex.py:72-76: >= L*K darts and every bucket >= K
+            if (full == (unsigned)L) {  // implies >= L*K darts
+              status = DSK_OK;
+              phi_star = phi;
+              Lsel = Lim;
+              break;
+            }
+          }
+        }
+        if (err) {
+          // a failing first band at phi0 > 1: the host's retry launch redoes
+          // the set from phi = 1 (dsk_lsh_csr)
+          status = (phi == phi0 && phi0 > 1) ? DSK_RETRY : err;
+          break;
+        }
+        L_prev = Lim;
+        RD_prev = RD;
+      }
+    }
+    unsigned wd = __reduce_add_sync(DSK_FULL, n_darts), wh = __reduce_add_sync(DSK_FULL, n_hits);
+    if (lane == 0) { atomicAdd(&C.darts, wd); atomicAdd(&C.hits, wh); }
+    team_sync(G, team);
+    if (status == 0) {
+      LshSel x;
+      x.T = &T; x.smem = smem; x.C = &C; x.cnt = cnt; x.fullc = fullc; x.buf = buf; x.ovf = ovf;
+      x.ovf_b = ovf_b; x.sel = sel; x.gtab = a.tabs.tab; x.out_fps = a.out_fps;
+      x.out_keys = a.out_keys; x.s = s; x.Lsel = Lsel; x.L = L; x.K = K; x.G = G; x.team = team;
+      x.wit = wit; x.lane = lane; x.tt = tt; x.exact_sort = a.exact_sort; x.phi0 = a.phi0;
+      x.phi_star = phi_star; x.S = S; x.cap = a.cap;
+      phi_star = lsh_select(x);
     } else {
       for (int b = tt; b < L; b += G * 32) {
         if (a.out_keys) a.out_keys[(size_t)s * L + b] = 0;
