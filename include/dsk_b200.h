@@ -88,7 +88,9 @@ int dsk_minhash_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
 
 /* dsk_minhash_csr with a hint for the CTA shape: nnz_hint = total nonzeros
  * of the batch (0 = unknown).  Results are identical; only the team shape
- * (warps per set) depends on it. */
+ * (warps per set) depends on it: a large mean admits two-warp teams.  Pass 0
+ * for batches of mostly small sets (the facade and dsk_minhash_csr_host do so
+ * when half of ~4096 sampled rows hold < 48 elements). */
 int dsk_minhash_csr_ex(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
                        const double *weights, int64_t n, int32_t k, int64_t nnz_hint,
                        uint64_t *out_values, uint64_t *out_bits, int32_t *status, int32_t *phi,

@@ -1086,8 +1086,10 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
   if (t > INT32_MAX) return set_err(DSK_EUNSUPPORTED, "k too large");
   int NW = 0, G = 0;
   // sets of >= 96 elements on average keep two warps busy: allow teams of 2
-  // in a wider CTA (cfg5: 24 warps x teams of 2 is 15 % faster than 20 x 1;
-  // sets of 64 elements prefer single-warp teams)
+  // in a wider CTA (uniform 1024-element sets, k = 64/128: 24 x 2 is 4-5 %
+  // faster than 20 x 1; sets of 64 elements prefer single-warp teams).
+  // Callers withhold the hint for batches of mostly small sets (cfg5's Zipf
+  // sizes, median 2: 20 x 1 is 8-12 % faster than 24 x 2)
   const int wide_g = nnz_hint >= 96 * n ? 2 : 0;
   // slot arrays in shared memory; k too large for that -> global memory (L2)
   bool global_slots = false;
@@ -1492,6 +1494,17 @@ static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
   return rc;
 }
 
+// Half or more of (up to) 4096 evenly spaced rows hold < 48 elements.
+static bool dsk_rows_skewed(const int64_t *indptr, int64_t n) {
+  const int64_t samples = n < 4096 ? n : 4096;
+  int64_t small = 0;
+  for (int64_t q = 0; q < samples; q++) {
+    const int64_t r = q * n / samples;
+    small += indptr[r + 1] - indptr[r] < 48;
+  }
+  return 2 * small >= samples;
+}
+
 extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                                     const double *weights, int64_t n, int32_t k,
                                     uint64_t *out_values, uint64_t *out_bits, int32_t *status,
@@ -1522,8 +1535,13 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
   int32_t *ds = (int32_t *)(base + off_s);
   int32_t *dph = phi ? (int32_t *)(base + off_ph) : nullptr;
   uint32_t *dst = stats ? (uint32_t *)(base + off_st) : nullptr;
+  // shape hint: a batch where most sets are small (cfg5's Zipf sizes) runs
+  // best on single-warp teams even when its mean is large, so the hint is
+  // withheld (0) when half of ~4096 evenly spaced rows have < 48 elements
+  const bool skewed = dsk_rows_skewed(indptr, n);
   auto launch = [&](int64_t r0, int64_t m, cudaStream_t st) {
-    return dsk_minhash_csr_ex(c, dp + r0, di, dw, m, k, indptr[r0 + m] - indptr[r0],
+    return dsk_minhash_csr_ex(c, dp + r0, di, dw, m, k,
+                              skewed ? 0 : indptr[r0 + m] - indptr[r0],
                               dv ? dv + r0 * k : nullptr,
                            db ? db + r0 * words : nullptr, ds + r0, dph ? dph + r0 : nullptr,
                            dst ? dst + r0 * 4 : nullptr, st);
