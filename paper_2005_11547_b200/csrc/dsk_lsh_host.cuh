@@ -58,7 +58,9 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.indptr = indptr; a.ids = ids; a.w = weights; a.n = n; a.L = L; a.K = K;
   a.normalize = normalize;
   const char *ex = getenv("DSK_LSH_EXACT");
-  a.exact_sort = ex && atoi(ex) != 0; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
+  a.exact_sort = ex && atoi(ex) != 0;
+  const char *qs = getenv("DSK_LSH_QSHIFT");
+  a.qshift = qs ? (atoi(qs) < 0 ? 0 : (atoi(qs) > 26 ? 26 : atoi(qs))) : 0; a.tf = (double)t; a.inv_t = 1.0 / (double)t;
   a.phi0 = phi0;
   a.retry_rows = nullptr;
   a.retry_n = nullptr;

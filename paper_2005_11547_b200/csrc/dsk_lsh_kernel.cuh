@@ -92,6 +92,7 @@ struct LshArgs {
   int32_t L, K;
   int32_t normalize;
   int32_t exact_sort;  // 1: skip the float-key fast path (env DSK_LSH_EXACT=1; tests)
+  int32_t qshift;      // tests (env DSK_LSH_QSHIFT): coarser fixed-point sort keys, forcing collisions
   int32_t phi0;        // first band (0, phi0 / l1]; 2 when phi* = 1 is unlikely (large L)
   const uint32_t *retry_rows;  // second launch: rows whose first band failed (phi0 = 1)
   const unsigned *retry_n;
@@ -138,7 +139,7 @@ struct LshSel {
   uint64_t *out_fps, *out_keys;
   long long s;
   double Lsel;
-  int L, K, G, team, wit, lane, tt, exact_sort, phi0, phi_star;
+  int L, K, G, team, wit, lane, tt, exact_sort, qshift, phi0, phi_star;
   uint32_t S, cap;
 };
 
@@ -239,7 +240,7 @@ int lsh_select(const LshSel &x) {
             const unsigned i = lane + 32 * h;
             double qd = __dmul_rn(__longlong_as_double((long long)e[h].y), qscale);
             uint32_t q = qd < 67108863.0 ? (uint32_t)qd : 67108863u;
-            key[h] = i < nb ? (q << 6) | i : 0xffffffffu;
+            key[h] = i < nb ? ((q >> x.qshift) << 6) | i : 0xffffffffu;
           }
           if (nb <= 32) {
             for (int kk = 2; kk <= 32; kk <<= 1) {
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       x.T = &T; x.smem = smem; x.C = &C; x.cnt = cnt; x.fullc = fullc; x.buf = buf; x.ovf = ovf;
       x.ovf_b = ovf_b; x.sel = sel; x.gtab = a.tabs.tab; x.out_fps = a.out_fps;
       x.out_keys = a.out_keys; x.s = s; x.Lsel = Lsel; x.L = L; x.K = K; x.G = G; x.team = team;
-      x.wit = wit; x.lane = lane; x.tt = tt; x.exact_sort = a.exact_sort; x.phi0 = a.phi0;
+      x.wit = wit; x.lane = lane; x.tt = tt; x.exact_sort = a.exact_sort; x.qshift = a.qshift; x.phi0 = a.phi0;
       x.phi_star = phi_star; x.S = S; x.cap = a.cap;
       phi_star = lsh_select(x);
     } else {

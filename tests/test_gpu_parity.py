@@ -388,9 +388,10 @@ def test_lsh_small_shapes():
 
 @pytest.mark.parametrize("scale_exp", [None, -200])
 def test_lsh_sort_paths_agree(monkeypatch, scale_exp):
-    """The float-key bucket sort and the exact (rank, fp) sort give the same
-    keys.  With ||x||_1 = 2^-200 nearly every rank exceeds the float range,
-    so every bucket collides on its float keys and takes the exact path."""
+    """The fixed-point-key bucket sort and the exact (rank, fp) sort give the
+    same keys, also with ||x||_1 = 2^-200 (ranks far beyond the float range:
+    the keys are relative to the final limit).  Forced key collisions are
+    tested in test_round2.py::test_lsh_fixed_point_key_collisions."""
     indptr, ids, w = workloads.generate("cfg4", n=300, start=777)
     if scale_exp is not None:
         for s in range(indptr.size - 1):

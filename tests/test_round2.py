@@ -300,3 +300,43 @@ def test_l1_pairwise_all_small_and_deep_sizes():
     got = l1_batch(indptr, w).cpu().numpy()
     exp = np.array([float(np.sum(w[indptr[s]:indptr[s + 1]])) for s in range(lens.size)])
     assert np.array_equal(got, exp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("qshift", [14, 20, 26])
+@pytest.mark.parametrize("L,K", [(100, 20), (2, 3)])
+def test_lsh_fixed_point_key_collisions(monkeypatch, qshift, L, K):
+    """The K <= 32 selection sorts 32-bit keys {26-bit fixed-point rank, entry
+    index}; equal fixed-point ranks among the first K + 1 send the bucket to
+    the exact (rank bits, fp) sort.  Coarser keys (DSK_LSH_QSHIFT drops low
+    bits: 26 leaves none) force that fallback on some or every bucket; keys,
+    fingerprints, phi* (incl. the phi* = 1 recovery of (2, 3)) and H(phi*)
+    still equal the oracle's (ref/annindex.py:64-82)."""
+    from paper_2005_11547_b200 import HashFamily, LshParams, as_u64, lsh_batch
+    monkeypatch.setenv("DSK_LSH_QSHIFT", str(qshift))
+    monkeypatch.setenv("DSK_LSH_PHI0", "2")
+    indptr, ids, w = workloads.generate("cfg4", n=300, start=4321)
+    res = lsh_batch(indptr, ids, w, LshParams(L, K), HashFamily(3), fps=True)
+    keys, fps, status, phi, hits = Oracle(3).lsh_csr(indptr, ids, w, L, K, want_fps=True)
+    assert (status == 0).all() and (res.status.cpu().numpy() == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(as_u64(res.fps), fps)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+    assert np.array_equal(res.stats.cpu().numpy()[:, 2], hits)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("L,K", [(3, 700), (2, 1600)])
+def test_lsh_large_K_selection_staging(L, K):
+    """Large K: the selected fingerprints of one table fill the team's staged
+    rows in shared memory one table at a time (3, 700), or do not fit there
+    and go through the global selection buffer (2, 1600); buckets of > 64
+    entries take the counting rank.  Keys and fingerprints equal the oracle's."""
+    from paper_2005_11547_b200 import HashFamily, LshParams, as_u64, lsh_batch
+    indptr, ids, w = workloads.generate("cfg4", n=24, start=99)
+    res = lsh_batch(indptr, ids, w, LshParams(L, K), HashFamily(3), fps=True)
+    keys, fps, status, phi, hits = Oracle(3).lsh_csr(indptr, ids, w, L, K, want_fps=True)
+    assert (status == 0).all() and (res.status.cpu().numpy() == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(as_u64(res.fps), fps)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
