@@ -1093,7 +1093,9 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
   const int wide_g = nnz_hint >= 96 * n ? 2 : 0;
   // slot arrays in shared memory; k too large for that -> global memory (L2)
   bool global_slots = false;
-  if (!choose_shape(c, [&](int g, int nw) { return minhash_smem(k, g, nw); }, n, NW, G,
+  const char *gsl = getenv("DSK_GLOBAL_SLOTS");  // tuning/tests: slot arrays in global memory
+  if ((gsl && atoi(gsl) != 0) ||
+      !choose_shape(c, [&](int g, int nw) { return minhash_smem(k, g, nw); }, n, NW, G,
                     wide_g)) {
     global_slots = true;  // (instantiated for the 20-warp CTA only)
     if (!choose_shape(c, [&](int g, int nw) {

@@ -12,6 +12,9 @@
 #define DSK_LSH_PF 0  // 1: fetch the next bucket's hit slots into registers, 2/3: prefetch them to L2/L1
                         // (measured: 1 +9.6 % time from engine spills, 2/3 +0.9 %)
 #endif
+#ifndef DSK_LSH_SEL32
+#define DSK_LSH_SEL32 1  // buckets of 33..64 entries: threshold + compaction, then a 32-wide sort
+#endif
 #ifndef DSK_LSH_FAST
 #define DSK_LSH_FAST 1  // 0: exact sort only; 1: float-key sort + exact fallback; 2: timing only
 #endif
@@ -195,12 +198,15 @@ int lsh_select(const LshSel &x) {
     // queues, row stride K | 1 words (conflict-free column reads in the
     // epilogue); the global `sel` when one table does not fit
     const int KS = K | 1;
-    const int cap_s = (int)((size_t)G * kQBytes / 8);
+    // (the last 128 B of each warp's share are its compaction scratch words)
+    const int cap_s = (int)((size_t)G * (kQBytes - 128) / 8);
     const bool in_smem = DSK_LSH_SSEL && cap_s >= KS;
     // (a multiple of the team's thread count, so no epilogue round is partial)
     const int TB = in_smem ? (cap_s / KS >= G * 32 ? cap_s / KS / (G * 32) * (G * 32) : cap_s / KS) : L;
     const int rs = in_smem ? KS : K;
     uint64_t *sq = reinterpret_cast<uint64_t *>(smem + kOffQueues + (size_t)team * G * kQBytes);
+    uint32_t *scr = reinterpret_cast<uint32_t *>(smem + kOffQueues + (size_t)(team + 1) * G * kQBytes -
+                                                 (size_t)(wit + 1) * 128);
     bool tie = false;
     auto fetch = [&](int b, ulonglong2 (&e)[2]) {
       const unsigned nb = cnt[b];
@@ -242,15 +248,52 @@ int lsh_select(const LshSel &x) {
             uint32_t q = qd < 67108863.0 ? (uint32_t)qd : 67108863u;
             key[h] = i < nb ? ((q >> x.qshift) << 6) | i : 0xffffffffu;
           }
-          if (nb <= 32) {
+          auto sort32 = [&](uint32_t &v) {
             for (int kk = 2; kk <= 32; kk <<= 1) {
               for (int j = kk >> 1; j > 0; j >>= 1) {
-                uint32_t y = __shfl_xor_sync(DSK_FULL, key[0], j);
+                uint32_t y = __shfl_xor_sync(DSK_FULL, v, j);
                 bool take_min = ((lane & j) == 0) == ((lane & kk) == 0);
-                if (take_min == (y < key[0])) key[0] = y;
+                if (take_min == (y < v)) v = y;
               }
             }
-          } else {
+          };
+          bool sorted = false;
+          if (nb <= 32) {
+            sort32(key[0]);
+            sorted = true;
+          }
+#if DSK_LSH_SEL32
+          else if (K <= 31) {
+            // Only the K + 1 smallest keys matter: keep the keys below a q
+            // threshold sized from the bucket (one band's ranks are uniform:
+            // ~K + 6 of nb expected, widened / narrowed once), and when
+            // K + 1..32 survive, compact them into one register (through the
+            // warp's scratch words) and sort 32 instead of 64
+            float fq = (float)(K + 6) / (float)nb * 67108864.0f;
+            for (int att = 0; att < 2 && !sorted; att++) {
+              const uint32_t tq = fq < 67108863.0f ? (uint32_t)fq : 67108863u;
+              const uint32_t thr = ((tq >> x.qshift) << 6) | 63u;
+              const bool s0 = key[0] <= thr, s1 = key[1] <= thr;
+              const unsigned b0 = __ballot_sync(DSK_FULL, s0), b1 = __ballot_sync(DSK_FULL, s1);
+              const int n0 = __popc(b0), c = n0 + __popc(b1);
+              if (c >= K + 1 && c <= 32) {
+                const unsigned lt = (1u << lane) - 1u;
+                if (s0) scr[__popc(b0 & lt)] = key[0];
+                if (s1) scr[n0 + __popc(b1 & lt)] = key[1];
+                __syncwarp();
+                uint32_t v = lane < c ? scr[lane] : 0xffffffffu;
+                __syncwarp();
+                sort32(v);
+                key[0] = v;
+                key[1] = 0xffffffffu;  // positions 0..K all lie below the threshold
+                sorted = true;
+              } else {
+                fq = c < K + 1 ? fq * 1.5f : fq * 0.7f;
+              }
+            }
+          }
+#endif
+          if (!sorted) {
             for (int kk = 2; kk <= 64; kk <<= 1) {
               for (int j = kk >> 1; j > 0; j >>= 1) {
                 if (j == 32) {
