@@ -8,10 +8,6 @@
 #ifndef DSK_LSH_SSEL
 #define DSK_LSH_SSEL 1  // selections staged in the team's idle warp queues (shared memory; 5 % faster on cfg4)
 #endif
-#ifndef DSK_LSH_PF
-#define DSK_LSH_PF 0  // 1: fetch the next bucket's hit slots into registers, 2/3: prefetch them to L2/L1
-                        // (measured: 1 +9.6 % time from engine spills, 2/3 +0.9 %)
-#endif
 #ifndef DSK_LSH_SEL32
 #define DSK_LSH_SEL32 1  // buckets of 33..64 entries: threshold + compaction, then a 32-wide sort
 #endif
@@ -180,8 +176,9 @@ int lsh_select(const LshSel &x) {
     // above the entry's 6-bit index, so the sorted position names its entry
     // directly; when two of the first K + 1 sorted keys share q the bucket
     // is redone on the exact (rank bits, fp) pair.  Larger buckets rank
-    // each entry by counting.  (Fetching the next bucket's entries ahead,
-    // DSK_LSH_PF, costs more in engine register spills than it hides.)
+    // each entry by counting.  (Fetching the next bucket's entries ahead --
+    // into registers, by L1/L2 prefetch or by cp.async into shared memory --
+    // measured slower: profiles/r02/experiments.md.)
     //
     // phi* = 1 inside a phi0 = 2 first band: bucket b held >= K hits with
     // rank <= L1 = fl(1 / l1) iff its K-th smallest rank is <= L1; when all
@@ -220,24 +217,12 @@ int lsh_select(const LshSel &x) {
     for (int c0 = 0; c0 < L; c0 += TB) {
       const int c1 = c0 + TB < L ? c0 + TB : L;
       uint64_t *selp = in_smem ? sq : sel + (size_t)c0 * K;
-      ulonglong2 e[2], en[2];
-      if (fastK && c0 + wit < c1) fetch(c0 + wit, e);
+      ulonglong2 e[2];
       for (int b = c0 + wit; b < c1; b += G) {
         const unsigned nb = cnt[b];
         const size_t o = (size_t)b * S;  // bucket b's slots (nb <= 64 <= S on the register paths)
         uint64_t *row = selp + (size_t)(b - c0) * rs;
-        if (fastK && b + G < c1) { if (DSK_LSH_PF == 1) fetch(b + G, en); }
-        if (DSK_LSH_PF >= 2 && b + G < c1) {
-          // prefetch the next bucket's slot lines (no registers held)
-          const unsigned nn = cnt[b + G];
-          const unsigned lines = ((nn < 64 ? nn : 64) * 16 + 127) / 128;
-          if ((unsigned)lane < lines) {
-            const ulonglong2 *pa = buf + (size_t)(b + G) * S + 8 * lane;
-            if (DSK_LSH_PF == 2) asm volatile("prefetch.global.L2 [%0];" ::"l"(pa));
-            else asm volatile("prefetch.global.L1 [%0];" ::"l"(pa));
-          }
-        }
-        if (DSK_LSH_PF != 1 && fastK && b != c0 + wit) fetch(b, e);
+        if (fastK) fetch(b, e);
         bool exact = nb > 64 || !fast64;
         if (!exact && fastK) {
           uint32_t key[2];
@@ -475,7 +460,6 @@ int lsh_select(const LshSel &x) {
         const unsigned lines = ((nb < S ? nb : S) * 16 + 127) / 128;
         for (unsigned q = lane; q < lines; q += 32) l2_discard(buf + o + 8 * q);
 #endif
-        if (DSK_LSH_PF == 1 && fastK) { e[0] = en[0]; e[1] = en[1]; }
       }
       __threadfence_block();
       team_sync(G, team);
