@@ -454,18 +454,27 @@ def _dup_rows(p: torch.Tensor, i: torch.Tensor) -> np.ndarray:
     return torch.unique(sr[1:][dup]).cpu().numpy()
 
 
-def _shape_hint(p: torch.Tensor, i: torch.Tensor) -> int:
+def _shape_hint(indptr, p: torch.Tensor, i: torch.Tensor) -> int:
     """nnz hint for dsk_minhash_csr_ex's team shape: the batch's nonzeros,
     or 0 (no hint) when at least half of ~4096 evenly spaced rows hold < 48
     elements -- mostly-small batches (cfg5's Zipf sizes) run faster on
-    single-warp teams whatever their mean.  Results never depend on it."""
+    single-warp teams whatever their mean.  Results never depend on it.
+    Host indptr arrays are sampled on the host; device ones only for batches
+    of >= 4096 rows (one tiny reduction + sync), smaller batches keep the
+    mean-based hint (their shape follows the one-wave rule anyway)."""
     n = p.numel() - 1
     if n < 1:
         return 0
-    rows = torch.div(torch.arange(min(n, 4096), device=p.device) * n, min(n, 4096),
-                     rounding_mode="floor")
-    small = int(((p[rows + 1] - p[rows]) < 48).sum())
-    return 0 if 2 * small >= rows.numel() else i.numel()
+    m = min(n, 4096)
+    if isinstance(indptr, np.ndarray):
+        rows = np.arange(m, dtype=np.int64) * n // m
+        small = int(np.count_nonzero((indptr[rows + 1] - indptr[rows]) < 48))
+    elif n < 4096:
+        return i.numel()
+    else:
+        rows = torch.div(torch.arange(m, device=p.device) * n, m, rounding_mode="floor")
+        small = int(((p[rows + 1] - p[rows]) < 48).sum())
+    return 0 if 2 * small >= m else i.numel()
 
 
 def minhash_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, values: bool = True,
@@ -485,7 +494,7 @@ def minhash_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, values: b
     st = torch.empty((n, 4), dtype=torch.int32, device=dev) if stats else None
     with torch.cuda.device(dev):
         _lib.check(_lib.load().dsk_minhash_csr_ex(
-            hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, int(k), _shape_hint(p, i), _ptr(out_v),
+            hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, int(k), _shape_hint(indptr, p, i), _ptr(out_v),
             _ptr(out_b), _ptr(status), _ptr(phi), _ptr(st), _stream_ptr(dev)), "dsk_minhash_csr")
     res = MinhashBatch(out_v, out_b, status, phi, st)
     if check:
