@@ -1336,7 +1336,12 @@ static bool is_pinned(const void *p) {
 }
 
 // memcpy with the host's threads (pageable -> pinned staging)
+static int stage_threads();
+
 static void par_memcpy(void *dst, const void *src, size_t bytes, int threads) {
+  // (re-read per copy: concurrent host-buffer calls share the cores)
+  const int live = stage_threads();
+  threads = live < threads ? live : threads;
   const int64_t blocks = (int64_t)threads * 4;
   const size_t step = ((bytes + blocks - 1) / blocks + 63) & ~(size_t)63;
 #pragma omp parallel for num_threads(threads) schedule(static)
@@ -1346,11 +1351,26 @@ static void par_memcpy(void *dst, const void *src, size_t bytes, int threads) {
   }
 }
 
+// host-buffer calls in flight in this process (one per GPU under
+// shard.minhash_host_multi): the staging threads are shared among them
+static std::atomic<int> g_host_calls{0};
+
 static int stage_threads() {
   if (const char *e = getenv("DSK_HOST_THREADS")) return atoi(e) > 0 ? atoi(e) : 1;
   unsigned hw = std::thread::hardware_concurrency();
-  return hw ? (int)(hw < 16 ? hw : 16) : 8;
+  int t = hw ? (int)(hw < 16 ? hw : 16) : 8;
+  const int calls = g_host_calls.load();
+  if (calls > 1) {
+    const int share = hw ? (int)hw / calls : t / calls;  // the host's cores, split between the calls
+    t = share < t ? share : t;
+  }
+  return t > 0 ? t : 1;
 }
+
+struct HostCallScope {
+  HostCallScope() { g_host_calls.fetch_add(1); }
+  ~HostCallScope() { g_host_calls.fetch_sub(1); }
+};
 
 static int ensure_pin_stage(dsk_ctx *c, size_t bytes) {
   for (int b = 0; b < 2; b++)
@@ -1441,6 +1461,7 @@ static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
   // from pageable memory goes through the driver's own small bounce buffer
   // and measured 6x slower on cfg2)
   const bool stage = !(is_pinned(ids) && is_pinned(weights));
+  HostCallScope scope;  // counted while this call runs (thread split for concurrent calls)
   const int threads = stage_threads();
   if (stage) {
     int64_t mx = 0;

@@ -147,3 +147,22 @@ def test_bench_reference_arm_json_contract():
     assert line["value"] > 0 and line["higher_is_better"] is True
     assert line["cpu_baseline"]["kind"] in ("reference", "port") and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def test_shape_hint_withheld_for_mostly_small_batches():
+    """dsk_minhash_csr_ex's team-shape hint (results never depend on it): the
+    batch's nonzeros for uniform large sets, 0 when half of the sampled rows
+    hold < 48 elements (cfg5's Zipf sizes run faster on single-warp teams)."""
+    import torch
+    from paper_2005_11547_b200.api import _shape_hint
+    from paper_2005_11547_b200 import workloads
+    for name, want_zero in (("cfg2", False), ("cfg5", True)):
+        indptr, ids, _ = workloads.generate(name, n=5000)
+        p = torch.from_numpy(indptr)
+        i = torch.from_numpy(ids.view(np.int64))
+        hint_host = _shape_hint(indptr, p, i)
+        hint_dev = _shape_hint(p, p, i)  # tensor path (device sample) on CPU tensors
+        assert hint_host == hint_dev
+        assert (hint_host == 0) == want_zero
+        if not want_zero:
+            assert hint_host == int(indptr[-1])

@@ -340,3 +340,55 @@ def test_lsh_large_K_selection_staging(L, K):
     assert np.array_equal(as_u64(res.keys), keys)
     assert np.array_equal(as_u64(res.fps), fps)
     assert np.array_equal(res.phi.cpu().numpy(), phi)
+
+
+@pytest.mark.gpu
+def test_concurrent_host_calls_on_separate_contexts():
+    """Three dsk_minhash_csr_host calls from three host threads, each on its
+    own context (as shard.minhash_host_multi drives one context per GPU; here
+    all on device 0), with pageable inputs so the host staging threads are
+    shared between the concurrent calls: the disjoint output slices equal one
+    device launch over the whole batch."""
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    import torch
+    from paper_2005_11547_b200 import HashFamily, _lib, as_u64, constants, minhash_batch
+    indptr, ids, w = workloads.generate("cfg2", n=3000, start=500)
+    f = HashFamily(1)
+    ref = minhash_batch(indptr, ids, w, 256, f, bits=True)
+    lib = _lib.load()
+    thr = constants.log2_thresholds()
+    ctxs = []
+    for _ in range(3):
+        out = ctypes.c_void_p()
+        _lib.check(lib.dsk_ctx_create(0, f._tables.ctypes.data, f.poisson_cdf.ctypes.data,
+                                      thr.ctypes.data, ctypes.byref(out)), "dsk_ctx_create")
+        ctxs.append(out)
+    n, k = indptr.size - 1, 256
+    values = np.zeros((n, k), dtype=np.uint64)
+    bits = np.zeros((n, 4), dtype=np.uint64)
+    status = np.zeros(n, dtype=np.int32)
+    bounds = [0, 1000, 2000, n]
+    P = ctypes.c_void_p
+
+    def run(r):
+        r0, r1 = bounds[r], bounds[r + 1]
+        e0 = int(indptr[r0])
+        local = np.ascontiguousarray(indptr[r0:r1 + 1] - e0)
+        with torch.cuda.device(0):
+            return lib.dsk_minhash_csr_host(
+                ctxs[r], P(local.ctypes.data), P(ids.ctypes.data + 8 * e0),
+                P(w.ctypes.data + 8 * e0), r1 - r0, k, P(values.ctypes.data + 8 * k * r0),
+                P(bits.ctypes.data + 8 * 4 * r0), P(status.ctypes.data + 4 * r0), None, None)
+
+    try:
+        with ThreadPoolExecutor(max_workers=3) as pool:
+            rcs = list(pool.map(run, range(3)))
+    finally:
+        for c in ctxs:
+            lib.dsk_ctx_destroy(c)
+    assert rcs == [0, 0, 0]
+    assert (status == 0).all()
+    assert np.array_equal(values, as_u64(ref.values))
+    assert np.array_equal(bits, as_u64(ref.bits))
