@@ -224,7 +224,11 @@ __device__ __forceinline__ uint32_t add_sat(uint32_t a, uint32_t b) {
   return (r < a || r > 0x80000000u) ? 0x80000000u : r;
 }
 
-template <class Sink, bool kFull>
+// kDirect: a specialisation for passes whose rank depth is 0 (every area
+// has rho = 0: the direct walkers only); the region stages and their state
+// compile away.  A pass that does not qualify sets `not_direct` and runs
+// nothing (the caller redoes the set with the general engine).
+template <class Sink, bool kFull, bool kDirect = false>
 struct Engine {
   const SmemTables &T;
   WarpQueues &Q;
@@ -240,6 +244,7 @@ struct Engine {
   bool use_table = false;
   bool direct = false;      // rho = 0 areas come from per-lane walkers, not the region ring
   bool abort = false;       // warp-uniform: area cap exceeded by one lane's share
+  bool not_direct = false;  // kDirect: this pass needs the general engine
   // per lane: areas of the full (non-band) step (area cap); saturates at
   // 2^31, far above the 2^27 cap, so sums stay exact wherever they matter
   uint32_t lane_full = 0;
@@ -302,6 +307,10 @@ struct Engine {
       direct = DSK_DIRECT && (P.RD == 0 || DSK_DIRECT == 2) && __all_sync(DSK_FULL, narrow) &&
                carry_a < (1u << 30) &&
                carry_f < (1u << 30);
+    }
+    if (kDirect) {
+      not_direct = !(use_table && direct && P.RD == 0);
+      direct = true;
     }
     __syncwarp();
   }
@@ -756,6 +765,7 @@ struct Engine {
   // warp's next chunk and returns false (warp-uniformly) when none is left.
   template <class ChunkFn>
   __device__ void run(ChunkFn next_chunk) {
+    if (kDirect && not_direct) return;
     bool el_done = false;
     for (;;) {
       const bool up_area_empty = el_done && rg_cnt == 0;
@@ -764,12 +774,12 @@ struct Engine {
         hits_step();
       } else if (ar_cnt >= DSK_TH_AREA || (up_area_empty && ar_cnt > 0)) {
         areas_step();
-      } else if (rg_cnt >= DSK_TH_REG || (el_done && rg_cnt > 0)) {
+      } else if (!kDirect && (rg_cnt >= DSK_TH_REG || (el_done && rg_cnt > 0))) {
         regions_step();
       } else if (!el_done) {
         if (direct && walkers_busy()) {
           direct_step();
-        } else if (el_cur < el_total) {
+        } else if (!kDirect && el_cur < el_total) {
           element_step();
           if (abort) return;
         } else {

@@ -33,6 +33,9 @@
 #ifndef DSK_LPT
 #define DSK_LPT 1  // largest-first row order for multi-wave minhash launches
 #endif
+#ifndef DSK_LSH_DIRECT_KERNEL
+#define DSK_LSH_DIRECT_KERNEL 1  // LSH first launch on the direct-only engine specialisation
+#endif
 #ifndef DSK_OPAQUE_TB
 #define DSK_OPAQUE_TB 1  // LSH team block offsets opaque to the compiler (no rematerialisation)
 #endif
@@ -327,7 +330,7 @@ __device__ void set_prologue(const double *w, double tf, const SmemTables &T, Te
   }
 }
 
-template <class Sink>
+template <class Sink, bool kDirect = false>
 __device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const PassParams &P,
                          const uint64_t *ids, const double *w, int64_t lo, int64_t nnz, int G,
                          int wit, int lane, double tf, TeamCtl &C, uint32_t &n_darts,
@@ -335,7 +338,11 @@ __device__ void run_pass(const SmemTables &T, WarpQueues &Q, Sink &sink, const P
   int64_t next_chunk = 0;
   C.pp = P;
   __syncwarp();
-  Engine<Sink, false> eng(T, Q, team_rwin(&C), sink, C.pp, lane);
+  Engine<Sink, false, kDirect> eng(T, Q, team_rwin(&C), sink, C.pp, lane);
+  if (kDirect && eng.not_direct) {  // (warp-uniform; every warp of the team agrees)
+    if (lane == 0) atomicOr(&C.abort, 2);
+    return;
+  }
   // element chunks are handed out dynamically to the team's warps; small sets
   // use narrower chunks so every warp of the team gets elements
   const int CH = (G == 1 || nnz >= 64 * G) ? 32 : (32 / G > 4 ? 32 / G : 4);
@@ -893,6 +900,8 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
   CUDA_TRY(bottomk_set_smem(smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<22>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -70,9 +70,17 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
   a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap; a.S = S;
   a.tabs = table_args(c, (double)t);
+  // the first launch runs the direct-only engine when its sets are likely to
+  // qualify (no normalisation: l1 ~ sum of raw weights) and a retry launch
+  // follows anyway (phi0 = 2); DSK_LSH_DIRECT=0 disables it (tests)
+  const char *dk = getenv("DSK_LSH_DIRECT");
+  bool direct_first = DSK_LSH_DIRECT_KERNEL && !gc && NW == 24 && phi0 > 1 && !normalize &&
+                      !(dk && atoi(dk) == 0);
   auto launch = [&]() {
     if (gc) {
       lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);
+    } else if (direct_first) {
+      lsh_kernel<24, false, true><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a);
     } else {
       switch (NW) {
         case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;
@@ -99,6 +107,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     a.phi0 = 1;
     a.retry_rows = rows;
     a.retry_n = cnt;
+    direct_first = false;  // the retry launch runs the general engine
     launch();
     CUDA_TRY(cudaGetLastError());
   }

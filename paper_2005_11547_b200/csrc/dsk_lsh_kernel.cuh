@@ -521,7 +521,11 @@ int lsh_select(const LshSel &x) {
 
 // kGC: the per-bucket counters live in the team's global scratch instead of
 // shared memory (L too large for shared memory; instantiated for NW = 20)
-template <int NW, bool kGC = false>
+// kDirect: the first launch of a batch without normalisation runs the
+// direct-only engine (rank depth 0 in every band: cfg4's (0, 2/l1] with
+// l1 ~ 200); a set with a band that needs the region stages is handed to the
+// retry launch (general engine, from phi = 1) like a failed first band.
+template <int NW, bool kGC = false, bool kDirect = false>
 __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = g_tabs;
@@ -640,7 +644,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           poisson_regs(P, T);
           const int par = phi & 1;
           team_sync(G, team);
-          run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
+          run_pass<LshSink, kDirect>(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
                    par, sexp);
           team_sync(G, team);
           const double areas = C.areas[par];
@@ -650,7 +654,8 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
           for (int i = tt; i < L; i += G * 32) off[i] = cnt[i];  // band snapshot
           team_sync(G, team);
-          if (ab || areas > kMaxAreas) err = DSK_AREAS;  // ref/darthash.py:243
+          if (kDirect && (C.abort & 2)) err = DSK_RETRY;  // needs the general engine
+          else if (ab || areas > kMaxAreas) err = DSK_AREAS;  // ref/darthash.py:243
           else if (ovf) err = DSK_SCRATCH;
           else if (a.force_retry && phi == phi0 && phi0 > 1) err = DSK_RETRY;  // tests
           if (!err) {
@@ -667,7 +672,7 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
         if (err) {
           // a failing first band at phi0 > 1: the host's retry launch redoes
           // the set from phi = 1 (dsk_lsh_csr)
-          status = (phi == phi0 && phi0 > 1) ? DSK_RETRY : err;
+          status = ((phi == phi0 && phi0 > 1) || err == DSK_RETRY) ? DSK_RETRY : err;
           break;
         }
         L_prev = Lim;

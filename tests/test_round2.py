@@ -392,3 +392,30 @@ def test_concurrent_host_calls_on_separate_contexts():
     assert (status == 0).all()
     assert np.array_equal(values, as_u64(ref.values))
     assert np.array_equal(bits, as_u64(ref.bits))
+
+
+@pytest.mark.gpu
+def test_lsh_direct_engine_and_handoff(monkeypatch):
+    """The LSH first launch runs the direct-only engine specialisation (rank
+    depth 0); sets whose band needs the region stages (here every other row
+    rescaled to ||x||_1 in [1, 2): limit 2 / l1 > 1, rank depth 1) are handed
+    to the general-engine retry launch.  Keys, fingerprints, phi* and H(phi*)
+    equal the oracle's and the general-engine-only run (DSK_LSH_DIRECT=0)."""
+    from paper_2005_11547_b200 import HashFamily, LshParams, as_u64, lsh_batch
+    indptr, ids, w = workloads.generate("cfg4", n=400, start=8000)
+    w = w.copy()
+    for s in range(0, indptr.size - 1, 2):
+        a, b = indptr[s], indptr[s + 1]
+        w[a:b] = w[a:b] / w[a:b].sum() * 1.5
+    f = HashFamily(3)
+    res = lsh_batch(indptr, ids, w, LshParams(100, 20), f, fps=True)
+    keys, fps, status, phi, hits = Oracle(3).lsh_csr(indptr, ids, w, 100, 20, want_fps=True)
+    assert (status == 0).all() and (res.status.cpu().numpy() == 0).all()
+    assert np.array_equal(as_u64(res.keys), keys)
+    assert np.array_equal(as_u64(res.fps), fps)
+    assert np.array_equal(res.phi.cpu().numpy(), phi)
+    assert np.array_equal(res.stats.cpu().numpy()[:, 2], hits)
+    monkeypatch.setenv("DSK_LSH_DIRECT", "0")
+    gen = lsh_batch(indptr, ids, w, LshParams(100, 20), f, fps=True)
+    assert np.array_equal(as_u64(gen.keys), keys)
+    assert np.array_equal(gen.stats.cpu().numpy(), res.stats.cpu().numpy())
