@@ -644,8 +644,10 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
           poisson_regs(P, T);
           const int par = phi & 1;
           team_sync(G, team);
-          run_pass<LshSink, kDirect>(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
-                   par, sexp);
+          if (!run_pass<LshSink, kDirect>(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C,
+                                          n_darts, n_hits, par, sexp) &&
+              tt == 0)
+            atomicOr(&C.abort, 2);  // kDirect: this band needs the general engine
           team_sync(G, team);
           const double areas = C.areas[par];
           const bool ab = C.abort != 0;
