@@ -86,10 +86,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) bottomk_kernel(BottomKArgs a) 
   unsigned long long *cursors = reinterpret_cast<unsigned long long *>(smem + kOffTeam);
   uint4 *rwin = reinterpret_cast<uint4 *>(smem + kOffTeam +
                                           align16(kWarps * sizeof(unsigned long long))) +
-                warp * kRwin;
+                warp * kRwinStride;
   PassParams *pps = reinterpret_cast<PassParams *>(
       smem + kOffTeam + align16(kWarps * sizeof(unsigned long long)) +
-      kWarps * kRwin * sizeof(uint4));
+      kWarps * kRwinStride * sizeof(uint4));
   BkEntry *buf = a.buf + ((size_t)blockIdx.x * kWarps + warp) * a.cap;
   const uint32_t k = (uint32_t)a.k;
   __syncthreads();
@@ -239,7 +239,7 @@ extern "C" int dsk_bottomk_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
   a.weight = weight; a.rank = rank; a.fp = fingerprint; a.status = status; a.phi = phi;
   a.tabs = table_args(c, (double)k);
   size_t smem = kOffTeam + align16(kWarps * sizeof(unsigned long long)) +
-                kWarps * kRwin * sizeof(uint4) + kWarps * sizeof(PassParams);
+                kWarps * kRwinStride * sizeof(uint4) + kWarps * sizeof(PassParams);
   bottomk_kernel<<<grid, kWarps * 32, smem, st>>>(a); count_launch();
   CUDA_TRY(cudaGetLastError());
   return scratch_release(c, slot, st);

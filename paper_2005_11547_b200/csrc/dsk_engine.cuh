@@ -58,6 +58,9 @@ namespace dsk {
 #ifndef DSK_REFILL
 #define DSK_REFILL 8
 #endif
+#ifndef DSK_SEEK_TAB
+#define DSK_SEEK_TAB 1  // walker seeks by table lookup for the first 256 areas of an element
+#endif
 #ifndef DSK_PT_IMM
 #define DSK_PT_IMM 1  // Poisson thresholds as immediates instead of shared-memory loads
 #endif
@@ -84,6 +87,8 @@ constexpr int kQ = 64 * kILP;   // hit ring capacity (>= kStep - 1 + kStep); pow
 constexpr int kJs = 64;      // folded (j, stream) table rows; Poisson counts < 64
 constexpr int kRwin = 64;    // per-pass rank-window table entries (nu, rho)
 constexpr int kRun = DSK_RUN;  // areas per walker run on the direct (rho = 0) path
+constexpr int kSeekTab = 256;  // walker seek table entries (per team, after the rank-window table)
+constexpr int kRwinStride = kRwin + kSeekTab / 16;  // uint4 units per rank-window block incl. the seek table
 
 struct SmemTables {
   uint64_t tE[8][256];    // T0..T7  element bytes
@@ -307,6 +312,23 @@ struct Engine {
       direct = DSK_DIRECT && (P.RD == 0 || DSK_DIRECT == 2) && __all_sync(DSK_FULL, narrow) &&
                carry_a < (1u << 30) &&
                carry_f < (1u << 30);
+#if DSK_SEEK_TAB
+      if (direct) {
+        // walker seek table: the nu of in-band area a of an element, for
+        // a < kSeekTab (smallest nu with inclusive prefix > a; the element's
+        // own dtop bounds a, so one table serves every element)
+        __syncwarp();
+        uint8_t *tab = seek_tab();
+        for (uint32_t a = lane; a < (uint32_t)kSeekTab && a < carry_a; a += 32) {
+          int lo = 0, hi = P.maxd;
+          while (lo < hi) {
+            int mid = (lo + hi) >> 1;
+            if (rwin[mid * rdp1].z > a) hi = mid; else lo = mid + 1;
+          }
+          tab[a] = (uint8_t)lo;
+        }
+      }
+#endif
     }
     if (kDirect) {
       not_direct = !(use_table && direct && P.RD == 0);
@@ -588,10 +610,19 @@ struct Engine {
   // Each lane walks a run of <= kRun consecutive rho = 0 areas of one element
   // (nu ascending, r ascending: the same areas the region ring would yield,
   // in any order), one area per step; idle lanes take the chunk's next runs.
+  __device__ __forceinline__ uint8_t *seek_tab() const {
+    return reinterpret_cast<uint8_t *>(rwin + kRwin);
+  }
+
   __device__ __forceinline__ void walker_seek(uint32_t a, int dtop) {
     // smallest nu <= dtop with inclusive prefix > a
     const int rdp1 = P.RD + 1;
     int lo = 0, hi = dtop;
+#if DSK_SEEK_TAB
+    if (a < (uint32_t)kSeekTab) {
+      lo = seek_tab()[a];
+    } else
+#endif
     while (lo < hi) {
       int mid = (lo + hi) >> 1;
       if (rwin[mid * rdp1].z > a) hi = mid; else lo = mid + 1;

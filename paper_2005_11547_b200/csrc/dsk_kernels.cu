@@ -202,8 +202,8 @@ struct TeamCtl {
   int overflow;        // LSH: hit buffer overflow
   PassParams pp;       // parameters of the current pass (identical writes by the team's warps)
 };
-// per-team block: control word + the per-pass rank-window table
-constexpr size_t kTeamCtlBytes = align16(sizeof(TeamCtl)) + kRwin * sizeof(uint4);
+// per-team block: control word + the per-pass rank-window table + walker seek table
+constexpr size_t kTeamCtlBytes = align16(sizeof(TeamCtl)) + kRwin * sizeof(uint4) + kSeekTab;
 __device__ __forceinline__ uint4 *team_rwin(TeamCtl *C) {
   return reinterpret_cast<uint4 *>(reinterpret_cast<unsigned char *>(C) + align16(sizeof(TeamCtl)));
 }
@@ -599,10 +599,10 @@ __global__ void __launch_bounds__(kWarps * 32, 1) darts_kernel(DartsArgs a) {
       reinterpret_cast<unsigned long long *>(smem + kOffTeam);
   uint4 *rwin = reinterpret_cast<uint4 *>(smem + kOffTeam +
                                           align16(kWarps * sizeof(unsigned long long))) +
-                warp * kRwin;
+                warp * kRwinStride;
   PassParams *pps = reinterpret_cast<PassParams *>(
       smem + kOffTeam + align16(kWarps * sizeof(unsigned long long)) +
-      kWarps * kRwin * sizeof(uint4));
+      kWarps * kRwinStride * sizeof(uint4));
   __syncthreads();
   for (int64_t s = (int64_t)blockIdx.x * kWarps + warp; s < a.n; s += (int64_t)gridDim.x * kWarps) {
     const int64_t lo = a.indptr[s], nnz = a.indptr[s + 1] - lo;
@@ -1190,7 +1190,7 @@ extern "C" int dsk_darts_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *
   a.rr = r; a.jj = j; a.weight = weight; a.rank = rank; a.fp = fingerprint;
   a.tabs = table_args(c, (double)t);
   size_t smem = kOffTeam + align16(kWarps * sizeof(unsigned long long)) +
-                kWarps * kRwin * sizeof(uint4) + kWarps * sizeof(PassParams);
+                kWarps * kRwinStride * sizeof(uint4) + kWarps * sizeof(PassParams);
   int grid = (int)((n + kWarps - 1) / kWarps);
   if (grid > c->num_sms) grid = c->num_sms;
   darts_kernel<<<grid, kWarps * 32, smem, st>>>(a); count_launch();
