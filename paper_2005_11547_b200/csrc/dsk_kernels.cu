@@ -903,6 +903,10 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<24, false, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<26, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<28, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<20, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(lsh_kernel<22>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -21,7 +21,31 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   }
   cudaStream_t st = (cudaStream_t)stream;
   CUDA_TRY(cudaSetDevice(c->device));
-  const int teams = NW / G;
+  // phi0 = 2 when every one of L >= 8 buckets rarely fills at phi = 1
+  // (P(all L buckets >= K) <= 0.63^L; cfg4: phi* = 2 or 3 for every set)
+  int phi0 = L >= 8 ? 2 : 1;
+  if (const char *e = getenv("DSK_LSH_PHI0")) phi0 = atoi(e) == 2 ? 2 : 1;
+  // the first launch runs the direct-only engine when its sets are likely to
+  // qualify (no normalisation: l1 ~ sum of raw weights) and a retry launch
+  // follows anyway (phi0 = 2); DSK_LSH_DIRECT=0 disables it (tests).  Without
+  // the region rings its queue blocks pack tighter, so it runs on the widest
+  // CTA that fits shared memory and the 16 named barriers: 28 warps (72
+  // registers per thread) in teams of 2 for cfg4, against 24 for the general
+  // engine (DSK_LSH_DNW: tuning)
+  const char *dk = getenv("DSK_LSH_DIRECT");
+  bool direct_first = DSK_LSH_DIRECT_KERNEL && !gc && NW == 24 && phi0 > 1 && !normalize &&
+                      !(dk && atoi(dk) == 0);
+  int DNW = NW;  // CTA width of the first launch
+  if (direct_first) {
+    const char *e = getenv("DSK_LSH_DNW");
+    const int want = e ? atoi(e) : 28;
+    for (int nw : {28, 26, 24})
+      if (nw <= want && nw % G == 0 && nw / G + 1 <= 16 && lsh_smem(L, G, nw, true) <= c->max_smem) {
+        DNW = nw;
+        break;
+      }
+  }
+  const int teams = DNW / G;  // (>= the retry launch's NW / G: scratch is sized for it)
   int grid = c->num_sms;
   if ((int64_t)grid * teams > n) grid = (int)((n + teams - 1) / teams);
   // hit slots per bucket: >= 64 (the register sorts) and >= about two bands
@@ -38,10 +62,6 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   size_t team_bytes = align128((size_t)L * S * 16) + align128((size_t)cap * 16) +
                       align128((size_t)cap * 4) + align128((size_t)L * K * 8) +
                       (gc ? align128(align16((size_t)3 * L * sizeof(unsigned)) + 16) : 0);
-  // phi0 = 2 when every one of L >= 8 buckets rarely fills at phi = 1
-  // (P(all L buckets >= K) <= 0.63^L; cfg4: phi* = 2 or 3 for every set)
-  int phi0 = L >= 8 ? 2 : 1;
-  if (const char *e = getenv("DSK_LSH_PHI0")) phi0 = atoi(e) == 2 ? 2 : 1;
   const size_t retry_off = (size_t)grid * teams * team_bytes;
   size_t need = retry_off + (phi0 > 1 ? align16((size_t)n * 4) + 16 : 0);
   // hit buffers from the context's stream-ordered scratch pool
@@ -70,17 +90,16 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   a.status = status; a.phi = phi; a.stats = stats; a.counter = counter;
   a.scratch = (unsigned char *)scratch; a.team_scratch = team_bytes; a.cap = cap; a.S = S;
   a.tabs = table_args(c, (double)t);
-  // the first launch runs the direct-only engine when its sets are likely to
-  // qualify (no normalisation: l1 ~ sum of raw weights) and a retry launch
-  // follows anyway (phi0 = 2); DSK_LSH_DIRECT=0 disables it (tests)
-  const char *dk = getenv("DSK_LSH_DIRECT");
-  bool direct_first = DSK_LSH_DIRECT_KERNEL && !gc && NW == 24 && phi0 > 1 && !normalize &&
-                      !(dk && atoi(dk) == 0);
   auto launch = [&]() {
     if (gc) {
       lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);
     } else if (direct_first) {
-      lsh_kernel<24, false, true><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a);
+      const size_t sm = lsh_smem(L, G, DNW, true);
+      switch (DNW) {
+        case 28: lsh_kernel<28, false, true><<<grid, 28 * 32, sm, st>>>(a); break;
+        case 26: lsh_kernel<26, false, true><<<grid, 26 * 32, sm, st>>>(a); break;
+        default: lsh_kernel<24, false, true><<<grid, 24 * 32, sm, st>>>(a); break;
+      }
     } else {
       switch (NW) {
         case 24: lsh_kernel<24><<<grid, 24 * 32, lsh_smem(L, G, NW), st>>>(a); break;

@@ -117,9 +117,20 @@ __host__ __device__ inline size_t lsh_team_bytes(int L) {
   return kTeamCtlBytes + align16((size_t)3 * L * sizeof(unsigned int)) + 16;
 }
 
-__host__ __device__ inline size_t lsh_smem(int L, int G, int nw) {
+// The direct-only engine never touches the region ring (the first
+// kQDirectSkip bytes of WarpQueues), so its kernel packs the warps' queue
+// blocks at a stride of kQBytes - kQDirectSkip: warp w's (unused) region ring
+// overlaps the tail of warp w - 1's block, and 28 warps fit where 24 did.
+constexpr size_t kQDirectSkip = offsetof(WarpQueues, arA);
+__host__ __device__ constexpr size_t lsh_qstride(bool direct) {
+  return direct ? kQBytes - kQDirectSkip : kQBytes;
+}
+__host__ __device__ constexpr size_t lsh_off_team(int nw, bool direct) {
+  return direct ? nw * lsh_qstride(true) + kQDirectSkip : off_team(nw);
+}
+__host__ __device__ inline size_t lsh_smem(int L, int G, int nw, bool direct = false) {
   int teams = nw / G;
-  return off_team(nw) + (size_t)teams * lsh_team_bytes(L);
+  return lsh_off_team(nw, direct) + (size_t)teams * lsh_team_bytes(L);
 }
 
 // Selection + epilogue of one set (ref/annindex.py:77-81, :135), kept out
@@ -140,6 +151,7 @@ struct LshSel {
   double Lsel;
   int L, K, G, team, wit, lane, tt, exact_sort, qshift, phi0, phi_star;
   uint32_t S, cap;
+  uint32_t sq_off, qstride;  // the team's staging area: the used part of its warps' queue blocks
 };
 
 #ifndef DSK_LSH_SEL_NOINLINE
@@ -196,13 +208,13 @@ int lsh_select(const LshSel &x) {
     // epilogue); the global `sel` when one table does not fit
     const int KS = K | 1;
     // (the last 128 B of each warp's share are its compaction scratch words)
-    const int cap_s = (int)((size_t)G * (kQBytes - 128) / 8);
+    const int cap_s = (int)((size_t)G * (x.qstride - 128) / 8);
     const bool in_smem = DSK_LSH_SSEL && cap_s >= KS;
     // (a multiple of the team's thread count, so no epilogue round is partial)
     const int TB = in_smem ? (cap_s / KS >= G * 32 ? cap_s / KS / (G * 32) * (G * 32) : cap_s / KS) : L;
     const int rs = in_smem ? KS : K;
-    uint64_t *sq = reinterpret_cast<uint64_t *>(smem + kOffQueues + (size_t)team * G * kQBytes);
-    uint32_t *scr = reinterpret_cast<uint32_t *>(smem + kOffQueues + (size_t)(team + 1) * G * kQBytes -
+    uint64_t *sq = reinterpret_cast<uint64_t *>(smem + x.sq_off);
+    uint32_t *scr = reinterpret_cast<uint32_t *>(smem + x.sq_off + (size_t)G * x.qstride -
                                                  (size_t)(wit + 1) * 128);
     bool tie = false;
     auto fetch = [&](int b, ulonglong2 (&e)[2]) {
@@ -534,12 +546,12 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
             tt = opaque_team(wit * 32 + lane);
   const int L = a.L, K = a.K;
-  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
+  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * lsh_qstride(kDirect));
   const size_t tbytes = kGC ? kTeamCtlBytes : lsh_team_bytes(L);
 #if DSK_OPAQUE_TB
-  unsigned char *tb = smem + opaque_int((int)(off_team(NW) + team * tbytes));
+  unsigned char *tb = smem + opaque_int((int)(lsh_off_team(NW, kDirect) + team * tbytes));
 #else
-  unsigned char *tb = smem + off_team(NW) + team * tbytes;
+  unsigned char *tb = smem + lsh_off_team(NW, kDirect) + team * tbytes;
 #endif
   TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
   // global scratch of this team
@@ -691,6 +703,9 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       x.out_keys = a.out_keys; x.s = s; x.Lsel = Lsel; x.L = L; x.K = K; x.G = G; x.team = team;
       x.wit = wit; x.lane = lane; x.tt = tt; x.exact_sort = a.exact_sort; x.qshift = a.qshift; x.phi0 = a.phi0;
       x.phi_star = phi_star; x.S = S; x.cap = a.cap;
+      x.qstride = (uint32_t)lsh_qstride(kDirect);
+      x.sq_off = (uint32_t)(kOffQueues + (size_t)team * G * lsh_qstride(kDirect) +
+                            (kDirect ? kQDirectSkip : 0));
       phi_star = lsh_select(x);
     } else {
       for (int b = tt; b < L; b += G * 32) {

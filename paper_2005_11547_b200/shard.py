@@ -148,6 +148,88 @@ def minhash_host_multi(indptr, ids, weights, k: int, hashes, *, devices=None, bi
     return values, packed, status
 
 
+def sharded_lsh(indptr, ids, weights, params, hashes, *, normalize: bool = False,
+                group=None, gather: bool = False):
+    """lsh_key + mix64 (ref/annindex.py:64-82, :135) for this rank's row range
+    on this rank's GPU; ranges are balanced on the dart density t = L * K.
+
+    Returns (bounds, LshBatch of the local rows[, gathered keys]).
+    """
+    from .api import lsh_batch
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    bounds = plan_shards(indptr, world, params.L * params.K)
+    p, i, w = shard_csr(indptr, ids, weights, bounds, rank)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    res = lsh_batch(p, i, w, params, hashes, normalize=normalize, device=dev)
+    if gather and world > 1:
+        return bounds, res, gather_rows(res.keys, bounds, group)
+    return bounds, res
+
+
+def lsh_host_multi(indptr, ids, weights, params, hashes, *, devices=None,
+                   normalize: bool = False, check: bool = True):
+    """(L, K) table keys for a CSR batch in host memory, row-sharded over
+    several GPUs driven by this one process -- minhash_host_multi's
+    counterpart for the LSH path (dsk_lsh_csr_host per device, each range
+    written into its slice of the host outputs; no collective).
+
+    Returns (keys uint64[n, L], status int32[n], phi int32[n]) as numpy arrays.
+    """
+    import ctypes
+    from concurrent.futures import ThreadPoolExecutor
+
+    from . import _lib
+    from .api import DSK_STATUS_TIE, as_u64, lsh_batch, raise_for_status
+    from .workloads import subset
+    L, K = int(params.L), int(params.K)
+    indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+    ids = np.ascontiguousarray(ids, dtype=np.uint64)
+    weights = np.ascontiguousarray(weights, dtype=np.float64)
+    n = indptr.size - 1
+    if devices is None:
+        devices = list(range(torch.cuda.device_count()))
+    devices = [int(d) for d in devices]
+    keys = np.zeros((n, L), dtype=np.uint64)
+    status = np.zeros(n, dtype=np.int32)
+    phi = np.zeros(n, dtype=np.int32)
+    bounds = plan_shards(indptr, len(devices), L * K)
+    ctxs = [hashes.context(torch.device("cuda", d)) for d in devices]  # created up front
+    lib = _lib.load()
+    P = ctypes.c_void_p
+
+    def run(r):
+        r0, r1 = int(bounds[r]), int(bounds[r + 1])
+        if r1 == r0:
+            return 0
+        e0 = int(indptr[r0])
+        local = np.ascontiguousarray(indptr[r0:r1 + 1] - e0)
+        with torch.cuda.device(devices[r]):
+            return lib.dsk_lsh_csr_host(
+                ctxs[r], P(local.ctypes.data), P(ids.ctypes.data + 8 * e0),
+                P(weights.ctypes.data + 8 * e0), r1 - r0, L, K, int(bool(normalize)),
+                P(keys.ctypes.data + 8 * L * r0), None, P(status.ctypes.data + 4 * r0),
+                P(phi.ctypes.data + 4 * r0), None)
+
+    with ThreadPoolExecutor(max_workers=len(devices)) as pool:
+        rcs = list(pool.map(run, range(len(devices))))
+    for rc in rcs:
+        _lib.check(rc, "dsk_lsh_csr_host")
+    if check:
+        raise_for_status(torch.from_numpy(status))
+        # rows with bit-identical ranks in a bucket: re-keyed by index tuple
+        # through lsh_batch's tie path (ref/annindex.py:77-81)
+        rows = np.nonzero((status & DSK_STATUS_TIE) != 0)[0]
+        if rows.size:
+            sp, si, sw = subset(indptr, ids, weights, rows)
+            res = lsh_batch(sp, si, sw, params, hashes, normalize=normalize, stats=False,
+                            device=torch.device("cuda", devices[0]))
+            keys[rows] = as_u64(res.keys)
+            status[rows] = res.status.cpu().numpy()
+            phi[rows] = res.phi.cpu().numpy()
+    return keys, status, phi
+
+
 def repair_tied_rows(indptr, ids, weights, k: int, hashes, values, packed, status, *,
                      device=0) -> int:
     """Re-resolve host-path rows flagged DSK_STATUS_TIE by full index tuple.

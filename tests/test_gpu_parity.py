@@ -424,6 +424,24 @@ def test_minhash_host_multi_device_gather():
         assert np.array_equal(bits, as_u64(dev.bits))
 
 
+@pytest.mark.parametrize("normalize", [False, True])
+def test_lsh_host_multi_device_gather(normalize):
+    """The LSH counterpart of minhash_host_multi: row shards through
+    dsk_lsh_csr_host into disjoint slices of the host outputs (three shards on
+    device 0 stand in for three GPUs), equal to one lsh_batch launch."""
+    from paper_2005_11547_b200.shard import lsh_host_multi
+    indptr, ids, w = workloads.generate("cfg4", n=1500, start=50)
+    f = fam(3)
+    prm = LshParams(100, 20)
+    dev = lsh_batch(indptr, ids, w, prm, f, normalize=normalize)
+    for devices in ([0], [0, 0, 0]):
+        keys, status, phi = lsh_host_multi(indptr, ids, w, prm, f, devices=devices,
+                                           normalize=normalize)
+        assert (status == 0).all()
+        assert np.array_equal(keys, as_u64(dev.keys))
+        assert np.array_equal(phi, dev.phi.cpu().numpy())
+
+
 @pytest.mark.parametrize("L,K", [(6000, 1), (5000, 2)])
 def test_lsh_large_L_global_counters_vs_oracle(L, K):
     """L beyond the shared-memory bucket counters: counters in global scratch."""

@@ -139,3 +139,56 @@ def test_rank_shards_byte_identical_to_one_launch_gloo():
     other) sketch their own cfg5 row ranges; the gathered values, 1-bit words
     and statuses are byte-identical to a single launch over all rows."""
     _run_ranks(2, use_gpu=True)
+
+
+def _lsh_rank_worker(rank, world, port, q):
+    """The headline LSH workload's multi-GPU data path: cfg4 rows planned from
+    the row lengths on t = L * K, each rank generating and keying only its own
+    rows; the gathered keys equal one launch over the whole batch."""
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2005_11547_b200 import HashFamily, LshParams, lsh_batch
+    n, prm = 3000, LshParams(100, 20)
+    lens = workloads.lengths("cfg4", n)
+    bounds = shard.plan_shards_lengths(lens, world, prm.L * prm.K)
+    r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+    p, i, w = workloads.generate("cfg4", n=r1 - r0, start=r0, workers=2)
+    res = lsh_batch(p, i, w, prm, HashFamily(3), device="cuda:0")
+    local = torch.cat([res.keys, res.phi.to(torch.int64).unsqueeze(1),
+                       res.status.to(torch.int64).unsqueeze(1)], dim=1).cpu()
+    full = shard.gather_rows(local, bounds)
+    ok = True
+    if rank == 0:
+        fp, fi, fw = workloads.generate("cfg4", n=n, workers=2)
+        one = lsh_batch(fp, fi, fw, prm, HashFamily(3), device="cuda:0")
+        ref = torch.cat([one.keys, one.phi.to(torch.int64).unsqueeze(1),
+                         one.status.to(torch.int64).unsqueeze(1)], dim=1).cpu()
+        ok = bool(torch.equal(full, ref))
+    q.put((rank, ok))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_lsh_rank_shards_byte_identical_to_one_launch_gloo():
+    """Two ranks (gloo, sharing the one GPU) key their own cfg4 row ranges; the
+    gathered LSH keys, phi* and statuses are byte-identical to a single launch."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_lsh_rank_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(ok for _, ok in res), res
+
+
+def test_plan_shards_lsh_density():
+    """LSH shards are balanced on t = L * K (the per-set term dominates for
+    cfg4's fixed-size sets: equal row counts up to one row)."""
+    lens = workloads.lengths("cfg4", 10001)
+    b = shard.plan_shards_lengths(lens, 8, 2000)
+    assert b[0] == 0 and b[-1] == 10001
+    assert np.diff(b).max() - np.diff(b).min() <= 1
