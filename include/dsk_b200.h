@@ -90,11 +90,27 @@ int dsk_minhash_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
  * of the batch (0 = unknown).  Results are identical; only the team shape
  * (warps per set) depends on it: a large mean admits two-warp teams.  Pass 0
  * for batches of mostly small sets (the facade and dsk_minhash_csr_host do so
- * when half of ~4096 sampled rows hold < 48 elements). */
+ * when half of ~4096 sampled rows hold < 48 elements).
+ * DSK_HINT_DIRECT or-ed into nnz_hint says that nearly every set has l1 > 2
+ * (every band up to phi = 2 has rank depth 0): large batches then run a
+ * first launch of the direct-only engine on a wider CTA and a second,
+ * general launch for the sets that need the region stages (10-12 % faster
+ * on cfg3; a batch of normalised sets would pay ~6 % for the hand-back, so
+ * the callers set it only when 90 % of 256 sampled rows qualify). */
+#define DSK_HINT_DIRECT ((int64_t)1 << 62)
 int dsk_minhash_csr_ex(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
                        const double *weights, int64_t n, int32_t k, int64_t nnz_hint,
                        uint64_t *out_values, uint64_t *out_bits, int32_t *status, int32_t *phi,
                        uint32_t *stats, void *stream);
+
+/* nnz_hint for dsk_minhash_csr_ex from device-resident CSR arrays, sampled on
+ * the device as dsk_minhash_csr_host samples its host arrays: `nnz` (or 0
+ * when half of ~4096 evenly spaced rows hold < 48 elements), with
+ * DSK_HINT_DIRECT when >= 90 % of 256 evenly spaced rows have l1 > 2.
+ * Batches of < 4096 rows return `nnz`.  Synchronises `stream` (one small
+ * launch and an 8-byte copy). */
+int dsk_minhash_hints(dsk_ctx *ctx, const int64_t *indptr, const double *weights, int64_t n,
+                      int64_t nnz, int64_t *hint, void *stream);
 
 /* The same call with HOST buffers: copies inputs in, sketches, copies the
  * results out, synchronously.  This is the drop-in a ctypes binding of the

@@ -454,27 +454,55 @@ def _dup_rows(p: torch.Tensor, i: torch.Tensor) -> np.ndarray:
     return torch.unique(sr[1:][dup]).cpu().numpy()
 
 
-def _shape_hint(indptr, p: torch.Tensor, i: torch.Tensor) -> int:
-    """nnz hint for dsk_minhash_csr_ex's team shape: the batch's nonzeros,
-    or 0 (no hint) when at least half of ~4096 evenly spaced rows hold < 48
-    elements -- mostly-small batches (cfg5's Zipf sizes) run faster on
-    single-warp teams whatever their mean.  Results never depend on it.
-    Host indptr arrays are sampled on the host; device ones only for batches
-    of >= 4096 rows (one tiny reduction + sync), smaller batches keep the
-    mean-based hint (their shape follows the one-wave rule anyway)."""
+HINT_DIRECT = 1 << 62  # DSK_HINT_DIRECT (include/dsk_b200.h)
+
+
+def _shape_hint(indptr, p: torch.Tensor, i: torch.Tensor, weights=None,
+                w: torch.Tensor | None = None) -> int:
+    """Hints for dsk_minhash_csr_ex (results never depend on them).
+
+    Team shape: the batch's nonzeros, or 0 (no hint) when at least half of
+    ~4096 evenly spaced rows hold < 48 elements -- mostly-small batches
+    (cfg5's Zipf sizes) run faster on single-warp teams whatever their mean.
+    Direct-first (bit 62): at least 90 % of 256 evenly spaced rows have
+    l1 > 2, so every band up to phi = 2 has rank depth 0 and the direct-only
+    first launch serves nearly every set (cfg3's raw weights: 10-12 % faster;
+    cfg2's normalised ones would all be handed back, so they do not get it).
+    Host arrays are sampled on the host; device ones only for batches of
+    >= 4096 rows (dsk_minhash_hints: one small launch + an 8-byte copy; this
+    function then returns -1), smaller batches keep the mean-based hint (their
+    shape follows the one-wave rule anyway)."""
     n = p.numel() - 1
     if n < 1:
         return 0
     m = min(n, 4096)
-    if isinstance(indptr, np.ndarray):
+    md = min(n, 256)
+    if isinstance(indptr, np.ndarray) and (weights is None or isinstance(weights, np.ndarray)):
         rows = np.arange(m, dtype=np.int64) * n // m
         small = int(np.count_nonzero((indptr[rows + 1] - indptr[rows]) < 48))
-    elif n < 4096:
-        return i.numel()
+        direct = 0
+        if weights is not None and n >= 4096:
+            for r in (np.arange(md, dtype=np.int64) * n // md).tolist():
+                direct += float(weights[indptr[r]:min(indptr[r + 1], indptr[r] + 4096)].sum()) > 2.0
     else:
-        rows = torch.div(torch.arange(m, device=p.device) * n, m, rounding_mode="floor")
-        small = int(((p[rows + 1] - p[rows]) < 48).sum())
-    return 0 if 2 * small >= m else i.numel()
+        return -1  # device arrays: dsk_minhash_hints samples them (minhash_batch)
+    hint = 0 if 2 * small >= m else i.numel()
+    if n >= 4096 and 10 * direct >= 9 * md:
+        hint |= HINT_DIRECT
+    return hint
+
+
+def _batch_hint(indptr, p, i, weights, w, hashes: "HashFamily", dev) -> int:
+    """_shape_hint, with device arrays sampled by dsk_minhash_hints."""
+    hint = _shape_hint(indptr, p, i, weights, w)
+    if hint < 0:
+        h = ctypes.c_int64(0)
+        with torch.cuda.device(dev):
+            _lib.check(_lib.load().dsk_minhash_hints(
+                hashes.context(dev), _ptr(p), _ptr(w), p.numel() - 1, i.numel(), ctypes.byref(h),
+                _stream_ptr(dev)), "dsk_minhash_hints")
+        hint = h.value
+    return hint
 
 
 def minhash_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, values: bool = True,
@@ -493,8 +521,9 @@ def minhash_batch(indptr, ids, weights, k: int, hashes: HashFamily, *, values: b
     phi = torch.empty(n, dtype=torch.int32, device=dev)
     st = torch.empty((n, 4), dtype=torch.int32, device=dev) if stats else None
     with torch.cuda.device(dev):
+        hint = _batch_hint(indptr, p, i, weights, w, hashes, dev)
         _lib.check(_lib.load().dsk_minhash_csr_ex(
-            hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, int(k), _shape_hint(indptr, p, i), _ptr(out_v),
+            hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, int(k), hint, _ptr(out_v),
             _ptr(out_b), _ptr(status), _ptr(phi), _ptr(st), _stream_ptr(dev)), "dsk_minhash_csr")
     res = MinhashBatch(out_v, out_b, status, phi, st)
     if check:

@@ -146,3 +146,55 @@ extern "C" int dsk_exact_jaccard(const int64_t *a_ptr, const uint64_t *a_ids, co
   CUDA_TRY(cudaGetLastError());
   return DSK_OK;
 }
+
+
+// ---- batch hints for dsk_minhash_csr_ex, sampled on the device ----------
+// out[0]: of min(n, 4096) evenly spaced rows, those holding < 48 elements;
+// out[1]: of min(n, 256) evenly spaced rows, those with l1 > 2 (plain sum of
+// the row's first 4096 weights: a lower bound, enough for the heuristic).
+__global__ void hint_sample_kernel(const int64_t *indptr, const double *w, int64_t n,
+                                   unsigned *out) {
+  const int tid = blockIdx.x * blockDim.x + threadIdx.x, lane = threadIdx.x & 31;
+  const int64_t m = n < 4096 ? n : 4096, md = n < 256 ? n : 256;
+  bool small = false;
+  if (tid < m) {
+    const int64_t r = (int64_t)tid * n / m;
+    small = indptr[r + 1] - indptr[r] < 48;
+  }
+  const unsigned sb = __ballot_sync(0xffffffffu, small);
+  if (lane == 0 && sb) atomicAdd(&out[0], (unsigned)__popc(sb));
+  const int warp = tid >> 5;
+  if (warp < md) {
+    const int64_t r = (int64_t)warp * n / md, lo = indptr[r];
+    int64_t len = indptr[r + 1] - lo;
+    len = len < 4096 ? len : 4096;
+    double s = 0.0;
+    for (int64_t e = lane; e < len; e += 32) s += w[lo + e];
+    for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0 && s > 2.0) atomicAdd(&out[1], 1u);
+  }
+}
+
+// nnz_hint for dsk_minhash_csr_ex from device-resident CSR arrays (what
+// dsk_minhash_csr_host derives from its host arrays): `nnz` or 0 for the team
+// shape, DSK_HINT_DIRECT when >= 90 % of the sampled rows have l1 > 2.  One
+// small launch, an 8-byte copy and a stream synchronise.
+extern "C" int dsk_minhash_hints(dsk_ctx *c, const int64_t *indptr, const double *weights,
+                                 int64_t n, int64_t nnz, int64_t *hint, void *stream) {
+  if (!c || !indptr || !hint || n < 0) return set_err(DSK_EARG, "bad argument");
+  *hint = nnz;
+  if (n < 4096 || !weights) return DSK_OK;  // small batches keep the mean-based hint
+  cudaStream_t st = (cudaStream_t)stream;
+  CUDA_TRY(cudaSetDevice(c->device));
+  std::lock_guard<std::mutex> lock(c->hint_mu);
+  CUDA_TRY(cudaMemsetAsync(c->d_hint, 0, 2 * sizeof(unsigned), st));
+  hint_sample_kernel<<<32, 256, 0, st>>>(indptr, weights, n, c->d_hint); count_launch();
+  CUDA_TRY(cudaGetLastError());
+  CUDA_TRY(cudaMemcpyAsync(c->h_hint, c->d_hint, 2 * sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t m = 4096, md = 256;
+  int64_t h = 2 * (int64_t)c->h_hint[0] >= m ? 0 : nnz;
+  if (10 * (int64_t)c->h_hint[1] >= 9 * md) h |= kMhDirectHint;
+  *hint = h;
+  return DSK_OK;
+}

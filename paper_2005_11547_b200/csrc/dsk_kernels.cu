@@ -53,6 +53,8 @@ struct dsk_ctx {
   uint64_t *d_pthr;    // 64
   double *d_l2thr;     // 258
   unsigned long long *d_counter;  // kCounterSlots work counters, one per in-flight launch
+  unsigned *d_hint = nullptr, *h_hint = nullptr;  // dsk_minhash_hints: device counters, pinned copy
+  std::mutex hint_mu;
   std::atomic<unsigned> next_slot{0};
   size_t max_smem;
   // host-buffer path: device staging owned by the context
@@ -183,6 +185,17 @@ constexpr size_t kOffTeam = kOffQueues + kWarps * kQBytes;
 // minhash / LSH kernels are instantiated for several CTA widths (warps per
 // CTA); the host picks per launch the width whose team size is smallest.
 __host__ __device__ constexpr size_t off_team(int nw) { return kOffQueues + nw * kQBytes; }
+// The direct-only engine never touches the region ring (the first
+// kQDirectSkip bytes of WarpQueues), so its kernels pack the warps' queue
+// blocks at a stride of kQBytes - kQDirectSkip: warp w's (unused) region ring
+// overlaps the tail of warp w - 1's block, and 28 warps fit where 22-24 did.
+constexpr size_t kQDirectSkip = offsetof(WarpQueues, arA);
+__host__ __device__ constexpr size_t q_stride(bool direct) {
+  return direct ? kQBytes - kQDirectSkip : kQBytes;
+}
+__host__ __device__ constexpr size_t off_team_x(int nw, bool direct) {
+  return direct ? kOffQueues + nw * q_stride(true) + kQDirectSkip : off_team(nw);
+}
 constexpr int kWidths[] = {24, 22, 20};
 
 struct TeamCtl {
@@ -286,6 +299,12 @@ struct MinhashArgs {
   uint64_t *gslots;  // non-null: slot arrays in global memory, 2*k words per team
   const uint32_t *order;  // non-null: rows in processing order (largest first)
   const unsigned *order_on;  // device flag: the order differs from the identity
+  // direct-only first launch: rows whose bands need the general engine are
+  // appended to retry_out; the second (general) launch works through them
+  uint32_t *retry_out;
+  unsigned *retry_out_n;
+  const uint32_t *retry_rows;
+  const unsigned *retry_n;
   TableArgs tabs;
 };
 
@@ -406,7 +425,10 @@ __device__ __forceinline__ int opaque_team(int v) {
   return v;
 }
 
-template <int NW, bool kGlobal = false>
+// kDirect: the direct-only engine specialisation (rank depth 0 in every
+// band) on packed queue blocks; a set with a band that needs the region
+// stages is appended to a.retry_out for the general-engine launch.
+template <int NW, bool kGlobal = false, bool kDirect = false>
 __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = g_tabs;
@@ -415,12 +437,14 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
             tt = opaque_team(wit * 32 + lane);
   const int k = a.k;
-  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * kQBytes);
-  TeamCtl &C = *reinterpret_cast<TeamCtl *>(smem + off_team(NW) + team * kTeamCtlBytes);
+  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * q_stride(kDirect));
+  TeamCtl &C =
+      *reinterpret_cast<TeamCtl *>(smem + off_team_x(NW, kDirect) + team * kTeamCtlBytes);
   const int teams = NW / G;
   uint64_t *slots =
       kGlobal ? a.gslots + ((size_t)blockIdx.x * teams + team) * 2 * (size_t)k
-              : reinterpret_cast<uint64_t *>(smem + off_team(NW) + teams * kTeamCtlBytes) +
+              : reinterpret_cast<uint64_t *>(smem + off_team_x(NW, kDirect) +
+                                             teams * kTeamCtlBytes) +
                     (size_t)team * 2 * k;
   __syncthreads();
 
@@ -433,7 +457,10 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   for (;;) {
     if (tt == 0) {
       long long q = (long long)atomicAdd(a.counter, 1ULL);
-      C.set = (a.order && q < a.n && *a.order_on) ? (long long)a.order[q] : q;
+      if (a.retry_rows)  // second launch: the rows the direct-only launch handed back
+        C.set = q < (long long)*a.retry_n ? (long long)a.retry_rows[q] : a.n;
+      else
+        C.set = (a.order && q < a.n && *a.order_on) ? (long long)a.order[q] : q;
     }
     team_sync(G, team);
     const long long s = C.set;
@@ -483,16 +510,20 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
         // (both engine specialisations inlined here, direct-only for rank
         // depth 0 passes, measured cfg3 -2.5 % but cfg2 / cfg5 +16 %: the
         // minhash kernel keeps the general engine)
-        run_pass(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit, lane, a.tf, C, n_darts, n_hits,
-                 par);
+        if (!run_pass<MinhashSink<kGlobal>, kDirect>(T, Q, sink, P, a.ids, a.w, lo, nnz, G, wit,
+                                                     lane, a.tf, C, n_darts, n_hits, par) &&
+            tt == 0)
+          atomicOr(&C.abort, 2);  // kDirect: this band needs the general engine
         team_sync(G, team);
         const double areas = C.areas[par];
         const bool ab = C.abort != 0;
+        const bool handoff = kDirect && (C.abort & 2);
         const unsigned filled = C.filled;
         // the other parity's counters were last read before the previous
         // barrier and are next written in the following pass
         if (tt == 0) { C.areas[par ^ 1] = 0.0; C.chunk[par ^ 1] = 0; }
         team_sync(G, team);
+        if (handoff) { status = DSK_RETRY; break; }
         if (ab || areas > kMaxAreas) { status = DSK_AREAS; break; }  // ref/darthash.py:243
         final_areas = areas;
         if (filled == (unsigned)k) {  // every bucket non-empty, ref/sketching.py:110
@@ -525,6 +556,8 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
       }
     }
     if (tt == 0) {
+      if (kDirect && status == DSK_RETRY && a.retry_out)
+        a.retry_out[atomicAdd(a.retry_out_n, 1u)] = (uint32_t)s;
       a.status[s] = status | (C.tie ? DSK_STATUS_TIE : 0);
       if (a.phi) a.phi[s] = phi_star;
       if (a.stats) {
@@ -843,9 +876,10 @@ __global__ void __launch_bounds__(512) hash_peak_kernel(const uint64_t *tab, int
 
 // ------------------------------------------------------------- host side
 
-static size_t minhash_smem(int k, int G, int nw, bool global_slots = false) {
+static size_t minhash_smem(int k, int G, int nw, bool global_slots = false, bool direct = false) {
   int teams = nw / G;
-  return off_team(nw) + teams * kTeamCtlBytes + (global_slots ? 0 : (size_t)teams * k * 16);
+  return off_team_x(nw, direct) + teams * kTeamCtlBytes +
+         (global_slots ? 0 : (size_t)teams * k * 16);
 }
 
 static cudaError_t bottomk_set_smem(int bytes);  // dsk_bottomk.cuh
@@ -885,6 +919,8 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
   CUDA_TRY(cudaMalloc(&c->d_pthr, 64 * sizeof(uint64_t)));
   CUDA_TRY(cudaMalloc(&c->d_l2thr, 258 * sizeof(double)));
   CUDA_TRY(cudaMalloc(&c->d_counter, kCounterSlots * sizeof(unsigned long long)));
+  CUDA_TRY(cudaMalloc(&c->d_hint, 2 * sizeof(unsigned)));
+  CUDA_TRY(cudaMallocHost(&c->h_hint, 2 * sizeof(unsigned)));
   CUDA_TRY(cudaMemcpy(c->d_tab, tables_host, 22 * 256 * sizeof(uint64_t), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c->d_pthr, pthr, sizeof(pthr), cudaMemcpyHostToDevice));
   CUDA_TRY(cudaMemcpy(c->d_l2thr, log2_thr_host, 258 * sizeof(double), cudaMemcpyHostToDevice));
@@ -894,6 +930,10 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<20>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<28, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<24, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<20, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(darts_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -924,6 +964,8 @@ extern "C" int dsk_ctx_destroy(dsk_ctx *c) {
   cudaFree(c->d_pthr);
   cudaFree(c->d_l2thr);
   cudaFree(c->d_counter);
+  cudaFree(c->d_hint);
+  cudaFreeHost(c->h_hint);
   if (c->stage) cudaFree(c->stage);
   for (int i = 0; i < dsk_ctx::kScratchSlots; i++) {
     if (c->scratch[i]) cudaFree(c->scratch[i]);
@@ -1089,6 +1131,9 @@ extern "C" int dsk_minhash_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t
                             stats, stream);
 }
 
+// bit 62 of dsk_minhash_csr_ex's nnz_hint
+constexpr int64_t kMhDirectHint = DSK_HINT_DIRECT;
+
 extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                                   const double *weights, int64_t n, int32_t k, int64_t nnz_hint,
                                   uint64_t *out_values, uint64_t *out_bits, int32_t *status,
@@ -1104,6 +1149,8 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
   // faster than 20 x 1; sets of 64 elements prefer single-warp teams).
   // Callers withhold the hint for batches of mostly small sets (cfg5's Zipf
   // sizes, median 2: 20 x 1 is 8-12 % faster than 24 x 2)
+  const bool direct_hint = (nnz_hint & kMhDirectHint) != 0;
+  nnz_hint &= ~kMhDirectHint;
   const int wide_g = nnz_hint >= 96 * n ? 2 : 0;
   // slot arrays in shared memory; k too large for that -> global memory (L2)
   bool global_slots = false;
@@ -1130,19 +1177,50 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
   a.gslots = nullptr;
   a.order = nullptr;
   a.order_on = nullptr;
+  a.retry_out = nullptr;
+  a.retry_out_n = nullptr;
+  a.retry_rows = nullptr;
+  a.retry_n = nullptr;
   size_t smem = minhash_smem(k, G, NW, global_slots);
   int grid = c->num_sms;
   if ((int64_t)grid * (NW / G) > n) grid = (int)((n + (NW / G) - 1) / (NW / G));
+  // Direct-first (kMhDirectHint in nnz_hint, or DSK_MH_DIRECT=1): the batch's
+  // sets mostly have l1 above their phi* (rank depth 0 in every band), so a
+  // first launch runs the direct-only engine on packed queue blocks -- the
+  // widest CTA in which the general shape's team size (or the next that
+  // fits) fits -- and appends the sets that need the region stages to a list
+  // the general-engine launch then works through.
+  int DNW = 0, DG = 0;
+  {
+    const char *e = getenv("DSK_MH_DIRECT");
+    bool want = e ? atoi(e) != 0 : direct_hint;
+    if (want && !global_slots && n >= 4 * (int64_t)grid * (NW / G) && n < (1LL << 32)) {
+      for (int nw : {28, 24}) {
+        if (nw < NW) break;
+        for (int g = G; g <= nw && !DNW; g++)
+          if (team_size_ok(g, nw) && minhash_smem(k, g, nw, false, true) <= c->max_smem) {
+            DNW = nw;
+            DG = g;
+          }
+        if (DNW) break;
+      }
+    }
+  }
+  const bool direct_first = DNW != 0;
   // largest-first order when the batch spans several waves of teams
   const bool lpt = DSK_LPT && n >= 4 * (int64_t)grid * (NW / G) && n < (1LL << 32);
   std::unique_lock<std::mutex> lock(c->scratch_mu, std::defer_lock);
   int slot = -1;
-  if (global_slots || lpt) {
+  uint32_t *retry_rows = nullptr;
+  unsigned *retry_cnt = nullptr;
+  if (global_slots || lpt || direct_first) {
     lock.lock();
     void *p = nullptr;
     const size_t slot_bytes = global_slots ? (size_t)grid * (NW / G) * 16 * (size_t)k : 0;
     const size_t order_off = align16(slot_bytes);
-    const size_t need = order_off + (lpt ? align16((size_t)n * 4) + 2 * kSizeClasses * 4 + 16 : 0);
+    const size_t retry_off =
+        order_off + (lpt ? align16((size_t)n * 4) + 2 * kSizeClasses * 4 + 16 : 0);
+    const size_t need = retry_off + (direct_first ? align16((size_t)n * 4) + 16 : 0);
     int rc = scratch_acquire(c, need, st, slot, p);
     if (rc) return rc;
     if (global_slots) a.gslots = (uint64_t *)p;
@@ -1156,6 +1234,32 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
       a.order = order;
       a.order_on = hist + 2 * kSizeClasses;
     }
+    if (direct_first) {
+      retry_rows = (uint32_t *)((char *)p + retry_off);
+      retry_cnt = (unsigned *)((char *)retry_rows + align16((size_t)n * 4));
+      CUDA_TRY(cudaMemsetAsync(retry_cnt, 0, sizeof(unsigned), st));
+    }
+  }
+  if (direct_first) {
+    MinhashArgs d = a;
+    d.G = DG;
+    d.retry_out = retry_rows;
+    d.retry_out_n = retry_cnt;
+    int dgrid = c->num_sms;
+    if ((int64_t)dgrid * (DNW / DG) > n) dgrid = (int)((n + (DNW / DG) - 1) / (DNW / DG));
+    const size_t dsm = minhash_smem(k, DG, DNW, false, true);
+    if (DNW == 28) minhash_kernel<28, false, true><<<dgrid, 28 * 32, dsm, st>>>(d);
+    else minhash_kernel<24, false, true><<<dgrid, 24 * 32, dsm, st>>>(d);
+    count_launch();
+    CUDA_TRY(cudaGetLastError());
+    // the general launch below takes the rows handed back (often none)
+    unsigned long long *counter2 = c->d_counter + (c->next_slot.fetch_add(1) % kCounterSlots);
+    CUDA_TRY(cudaMemsetAsync(counter2, 0, sizeof(unsigned long long), st));
+    a.counter = counter2;
+    a.order = nullptr;
+    a.order_on = nullptr;
+    a.retry_rows = retry_rows;
+    a.retry_n = retry_cnt;
   }
   if (global_slots) {
     minhash_kernel<20, true><<<grid, 20 * 32, smem, st>>>(a); count_launch();
@@ -1542,6 +1646,21 @@ static bool dsk_rows_skewed(const int64_t *indptr, int64_t n) {
   return 2 * small >= samples;
 }
 
+// At least 90 % of (up to) 256 evenly spaced rows have l1 > 2 (a plain sum is
+// enough for this heuristic): rank depth 0 in every band up to phi = 2, i.e.
+// the direct-only first launch serves nearly every set.
+static bool dsk_rows_direct(const int64_t *indptr, const double *w, int64_t n) {
+  const int64_t samples = n < 256 ? n : 256;
+  int64_t direct = 0;
+  for (int64_t q = 0; q < samples; q++) {
+    const int64_t r = q * n / samples;
+    double l1 = 0.0;
+    for (int64_t e = indptr[r]; e < indptr[r + 1] && !(l1 > 2.0); e++) l1 += w[e];
+    direct += l1 > 2.0;
+  }
+  return 10 * direct >= 9 * samples;
+}
+
 extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                                     const double *weights, int64_t n, int32_t k,
                                     uint64_t *out_values, uint64_t *out_bits, int32_t *status,
@@ -1576,9 +1695,12 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
   // best on single-warp teams even when its mean is large, so the hint is
   // withheld (0) when half of ~4096 evenly spaced rows have < 48 elements
   const bool skewed = dsk_rows_skewed(indptr, n);
+  // direct-first hint: nearly every sampled set has l1 > 2 (cfg3's raw
+  // weights; not cfg2's normalised ones)
+  const int64_t dhint = weights && dsk_rows_direct(indptr, weights, n) ? kMhDirectHint : 0;
   auto launch = [&](int64_t r0, int64_t m, cudaStream_t st) {
     return dsk_minhash_csr_ex(c, dp + r0, di, dw, m, k,
-                              skewed ? 0 : indptr[r0 + m] - indptr[r0],
+                              (skewed ? 0 : indptr[r0 + m] - indptr[r0]) | dhint,
                               dv ? dv + r0 * k : nullptr,
                            db ? db + r0 * words : nullptr, ds + r0, dph ? dph + r0 : nullptr,
                            dst ? dst + r0 * 4 : nullptr, st);

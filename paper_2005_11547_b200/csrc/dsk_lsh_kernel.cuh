@@ -117,20 +117,10 @@ __host__ __device__ inline size_t lsh_team_bytes(int L) {
   return kTeamCtlBytes + align16((size_t)3 * L * sizeof(unsigned int)) + 16;
 }
 
-// The direct-only engine never touches the region ring (the first
-// kQDirectSkip bytes of WarpQueues), so its kernel packs the warps' queue
-// blocks at a stride of kQBytes - kQDirectSkip: warp w's (unused) region ring
-// overlaps the tail of warp w - 1's block, and 28 warps fit where 24 did.
-constexpr size_t kQDirectSkip = offsetof(WarpQueues, arA);
-__host__ __device__ constexpr size_t lsh_qstride(bool direct) {
-  return direct ? kQBytes - kQDirectSkip : kQBytes;
-}
-__host__ __device__ constexpr size_t lsh_off_team(int nw, bool direct) {
-  return direct ? nw * lsh_qstride(true) + kQDirectSkip : off_team(nw);
-}
+// (the direct-only kernel packs its queue blocks: q_stride / off_team_x in dsk_kernels.cu)
 __host__ __device__ inline size_t lsh_smem(int L, int G, int nw, bool direct = false) {
   int teams = nw / G;
-  return lsh_off_team(nw, direct) + (size_t)teams * lsh_team_bytes(L);
+  return off_team_x(nw, direct) + (size_t)teams * lsh_team_bytes(L);
 }
 
 // Selection + epilogue of one set (ref/annindex.py:77-81, :135), kept out
@@ -546,12 +536,12 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
   const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
             tt = opaque_team(wit * 32 + lane);
   const int L = a.L, K = a.K;
-  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * lsh_qstride(kDirect));
+  WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * q_stride(kDirect));
   const size_t tbytes = kGC ? kTeamCtlBytes : lsh_team_bytes(L);
 #if DSK_OPAQUE_TB
-  unsigned char *tb = smem + opaque_int((int)(lsh_off_team(NW, kDirect) + team * tbytes));
+  unsigned char *tb = smem + opaque_int((int)(off_team_x(NW, kDirect) + team * tbytes));
 #else
-  unsigned char *tb = smem + lsh_off_team(NW, kDirect) + team * tbytes;
+  unsigned char *tb = smem + off_team_x(NW, kDirect) + team * tbytes;
 #endif
   TeamCtl &C = *reinterpret_cast<TeamCtl *>(tb);
   // global scratch of this team
@@ -703,8 +693,8 @@ __global__ void __launch_bounds__(NW * 32, 1) lsh_kernel(LshArgs a) {
       x.out_keys = a.out_keys; x.s = s; x.Lsel = Lsel; x.L = L; x.K = K; x.G = G; x.team = team;
       x.wit = wit; x.lane = lane; x.tt = tt; x.exact_sort = a.exact_sort; x.qshift = a.qshift; x.phi0 = a.phi0;
       x.phi_star = phi_star; x.S = S; x.cap = a.cap;
-      x.qstride = (uint32_t)lsh_qstride(kDirect);
-      x.sq_off = (uint32_t)(kOffQueues + (size_t)team * G * lsh_qstride(kDirect) +
+      x.qstride = (uint32_t)q_stride(kDirect);
+      x.sq_off = (uint32_t)(kOffQueues + (size_t)team * G * q_stride(kDirect) +
                             (kDirect ? kQDirectSkip : 0));
       phi_star = lsh_select(x);
     } else {

@@ -161,8 +161,16 @@ def test_shape_hint_withheld_for_mostly_small_batches():
         p = torch.from_numpy(indptr)
         i = torch.from_numpy(ids.view(np.int64))
         hint_host = _shape_hint(indptr, p, i)
-        hint_dev = _shape_hint(p, p, i)  # tensor path (device sample) on CPU tensors
-        assert hint_host == hint_dev
+        # tensor inputs are sampled on the device by dsk_minhash_hints (GPU test:
+        # test_minhash_direct_first_handoff checks both samples agree)
+        assert _shape_hint(p, p, i) == -1
         assert (hint_host == 0) == want_zero
         if not want_zero:
             assert hint_host == int(indptr[-1])
+    # direct-first bit: raw cfg3 weights (l1 ~ 32) qualify, cfg2's normalised ones do not
+    from paper_2005_11547_b200.api import HINT_DIRECT
+    for name, want in (("cfg3", True), ("cfg2", False)):
+        indptr, ids, w = workloads.generate(name, n=5000)
+        p = torch.from_numpy(indptr)
+        i = torch.from_numpy(ids.view(np.int64))
+        assert bool(_shape_hint(indptr, p, i, w) & HINT_DIRECT) == want

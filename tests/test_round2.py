@@ -419,3 +419,60 @@ def test_lsh_direct_engine_and_handoff(monkeypatch):
     gen = lsh_batch(indptr, ids, w, LshParams(100, 20), f, fps=True)
     assert np.array_equal(as_u64(gen.keys), keys)
     assert np.array_equal(gen.stats.cpu().numpy(), res.stats.cpu().numpy())
+
+
+@pytest.mark.gpu
+def test_minhash_direct_first_handoff(monkeypatch):
+    """Direct-first minhash (DSK_HINT_DIRECT): the direct-only launch sketches
+    the sets whose bands have rank depth 0 and hands the others (here every
+    third row, rescaled to l1 = 1 so that limit = phi / l1 >= 1) to the
+    general launch; values, bits, phi* and H(phi*) equal the plain path's and
+    the oracle's, whatever the hint."""
+    import torch
+    from paper_2005_11547_b200 import HashFamily, _lib, as_u64, minhash_batch
+    n, k = 20000, 64
+    indptr, ids, w = workloads.generate("cfg3", n=n, start=777)
+    w = w.copy()
+    for r in range(0, n, 3):
+        seg = slice(int(indptr[r]), int(indptr[r + 1]))
+        w[seg] /= w[seg].sum()
+    f = HashFamily(2)
+    monkeypatch.setenv("DSK_MH_DIRECT", "0")
+    plain = minhash_batch(indptr, ids, w, k, f, bits=True)
+    lib = _lib.load()
+    monkeypatch.setenv("DSK_MH_DIRECT", "1")
+    l0 = lib.dsk_launch_count()
+    res = minhash_batch(indptr, ids, w, k, f, bits=True)
+    torch.cuda.synchronize()
+    assert lib.dsk_launch_count() - l0 >= 2  # the direct-only launch + the general one
+    assert (res.status.cpu().numpy() == 0).all()
+    for a, b in ((res.values, plain.values), (res.bits, plain.bits), (res.phi, plain.phi),
+                 (res.stats[:, 2:], plain.stats[:, 2:])):
+        assert torch.equal(a, b)
+    rows = np.arange(0, n, 97)
+    sp, si, sw = workloads.subset(indptr, ids, w, rows)
+    vals, status, phi, _ = Oracle(2).minhash_csr(sp, si, sw, k)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(res.values)[rows], vals)
+    assert np.array_equal(res.phi.cpu().numpy()[rows], phi)
+    # the facade's own hint: raw cfg3 weights qualify, this mixed batch (a third
+    # of the rows normalised) does not
+    from paper_2005_11547_b200.api import HINT_DIRECT, _batch_hint
+    monkeypatch.delenv("DSK_MH_DIRECT")
+    dev = torch.device("cuda", 0)
+
+    def on_dev(*arrs):
+        return [torch.from_numpy(a.view(np.int64) if a.dtype == np.uint64 else a).to(dev)
+                for a in arrs]
+    p0, i0, w0 = workloads.generate("cfg3", n=8000)
+    tp, ti, tw = on_dev(p0, i0, w0)
+    assert _batch_hint(p0, tp, ti, w0, tw, f, dev) == (i0.size | HINT_DIRECT)  # host sample
+    assert _batch_hint(tp, tp, ti, tw, tw, f, dev) == (i0.size | HINT_DIRECT)  # device sample
+    tp, ti, tw = on_dev(indptr, ids, w)
+    assert _batch_hint(indptr, tp, ti, w, tw, f, dev) == ids.size
+    assert _batch_hint(tp, tp, ti, tw, tw, f, dev) == ids.size
+    # mostly-small rows: no team-shape hint either
+    p5, i5, w5 = workloads.generate("cfg5", n=8000)
+    tp, ti, tw = on_dev(p5, i5, w5)
+    assert _batch_hint(tp, tp, ti, tw, tw, f, dev) & ~HINT_DIRECT == 0
+    assert _batch_hint(p5, tp, ti, w5, tw, f, dev) == _batch_hint(tp, tp, ti, tw, tw, f, dev)
