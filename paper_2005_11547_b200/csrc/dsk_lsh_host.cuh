@@ -35,17 +35,28 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
   const char *dk = getenv("DSK_LSH_DIRECT");
   bool direct_first = DSK_LSH_DIRECT_KERNEL && !gc && NW == 24 && phi0 > 1 && !normalize &&
                       !(dk && atoi(dk) == 0);
-  int DNW = NW;  // CTA width of the first launch
+  int DNW = NW, DG = G;  // CTA width and team size of the first launch
   if (direct_first) {
     const char *e = getenv("DSK_LSH_DNW");
     const int want = e ? atoi(e) : 28;
-    for (int nw : {28, 26, 24})
-      if (nw <= want && nw % G == 0 && nw / G + 1 <= 16 && lsh_smem(L, G, nw, true) <= c->max_smem) {
-        DNW = nw;
-        break;
-      }
+    // multi-wave batches: single-warp teams when they fit (no team barriers,
+    // no chunk hand-out; cfg4: 28 x 1 is 3.6 % faster than 14 x 2), else the
+    // general shape's team size.  DSK_LSH_DG: tuning
+    const char *eg = getenv("DSK_LSH_DG");
+    int cand[2] = {n >= 4 * (int64_t)c->num_sms * 28 ? 1 : G, G};
+    if (eg && atoi(eg) >= 1) cand[0] = cand[1] = atoi(eg);
+    DNW = 0;
+    for (int q = 0; q < 2 && !DNW; q++)
+      for (int nw : {28, 26, 24})
+        if (nw <= want && team_size_ok(cand[q], nw) &&
+            lsh_smem(L, cand[q], nw, true) <= c->max_smem) {
+          DNW = nw;
+          DG = cand[q];
+          break;
+        }
+    if (!DNW) { DNW = NW; DG = G; direct_first = lsh_smem(L, G, NW, true) <= c->max_smem; }
   }
-  const int teams = DNW / G;  // (>= the retry launch's NW / G: scratch is sized for it)
+  const int teams = DNW / DG;  // (>= the retry launch's NW / G: scratch is sized for it)
   int grid = c->num_sms;
   if ((int64_t)grid * teams > n) grid = (int)((n + teams - 1) / teams);
   // hit slots per bucket: >= 64 (the register sorts) and >= about two bands
@@ -94,7 +105,8 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     if (gc) {
       lsh_kernel<20, true><<<grid, 20 * 32, off_team(20) + (size_t)teams * kTeamCtlBytes, st>>>(a);
     } else if (direct_first) {
-      const size_t sm = lsh_smem(L, G, DNW, true);
+      const size_t sm = lsh_smem(L, DG, DNW, true);
+      a.G = DG;
       switch (DNW) {
         case 28: lsh_kernel<28, false, true><<<grid, 28 * 32, sm, st>>>(a); break;
         case 26: lsh_kernel<26, false, true><<<grid, 26 * 32, sm, st>>>(a); break;
@@ -124,6 +136,7 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     CUDA_TRY(cudaMemsetAsync(counter2, 0, sizeof(unsigned long long), st));
     a.counter = counter2;
     a.phi0 = 1;
+    a.G = G;  // (the general shape)
     a.retry_rows = rows;
     a.retry_n = cnt;
     direct_first = false;  // the retry launch runs the general engine
