@@ -428,14 +428,17 @@ __device__ __forceinline__ int opaque_team(int v) {
 // kDirect: the direct-only engine specialisation (rank depth 0 in every
 // band) on packed queue blocks; a set with a band that needs the region
 // stages is appended to a.retry_out for the general-engine launch.
-template <int NW, bool kGlobal = false, bool kDirect = false>
+// kSingle: single-warp teams known at compile time (team = warp: no team
+// barriers or divisions by the team size left in the code; cfg5 -1.7 %)
+template <int NW, bool kGlobal = false, bool kDirect = false, bool kSingle = false>
 __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   extern __shared__ __align__(16) unsigned char smem[];
   SmemTables &T = g_tabs;
   load_tables(T, a.tabs);
   const int warp = opaque_int(threadIdx.x >> 5), lane = opaque_int(threadIdx.x & 31);
-  const int G = a.G, team = opaque_team(warp / G), wit = opaque_team(warp % G),
-            tt = opaque_team(wit * 32 + lane);
+  const int G = kSingle ? 1 : a.G, team = kSingle ? warp : opaque_team(warp / G),
+            wit = kSingle ? 0 : opaque_team(warp % G),
+            tt = kSingle ? lane : opaque_team(wit * 32 + lane);
   const int k = a.k;
   WarpQueues &Q = *reinterpret_cast<WarpQueues *>(smem + kOffQueues + warp * q_stride(kDirect));
   TeamCtl &C =
@@ -932,6 +935,12 @@ extern "C" int dsk_ctx_create(int device, const uint64_t *tables_host, const dou
                                 smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<28, false, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<28, false, true, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<20, false, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
+  CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<22, false, false, true>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<24, false, true>,
                                 cudaFuncAttributeMaxDynamicSharedMemorySize, smem_optin));
   CUDA_TRY(cudaFuncSetAttribute(minhash_kernel<20, true>,
@@ -1250,7 +1259,8 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
     int dgrid = c->num_sms;
     if ((int64_t)dgrid * (DNW / DG) > n) dgrid = (int)((n + (DNW / DG) - 1) / (DNW / DG));
     const size_t dsm = minhash_smem(k, DG, DNW, false, true);
-    if (DNW == 28) minhash_kernel<28, false, true><<<dgrid, 28 * 32, dsm, st>>>(d);
+    if (DNW == 28 && DG == 1) minhash_kernel<28, false, true, true><<<dgrid, 28 * 32, dsm, st>>>(d);
+    else if (DNW == 28) minhash_kernel<28, false, true><<<dgrid, 28 * 32, dsm, st>>>(d);
     else minhash_kernel<24, false, true><<<dgrid, 24 * 32, dsm, st>>>(d);
     count_launch();
     CUDA_TRY(cudaGetLastError());
@@ -1268,8 +1278,14 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
   } else {
     switch (NW) {
       case 24: minhash_kernel<24><<<grid, 24 * 32, smem, st>>>(a); break;
-      case 22: minhash_kernel<22><<<grid, 22 * 32, smem, st>>>(a); break;
-      default: minhash_kernel<20><<<grid, 20 * 32, smem, st>>>(a); break;
+      case 22:
+        if (G == 1) minhash_kernel<22, false, false, true><<<grid, 22 * 32, smem, st>>>(a);
+        else minhash_kernel<22><<<grid, 22 * 32, smem, st>>>(a);
+        break;
+      default:
+        if (G == 1) minhash_kernel<20, false, false, true><<<grid, 20 * 32, smem, st>>>(a);
+        else minhash_kernel<20><<<grid, 20 * 32, smem, st>>>(a);
+        break;
     }
     count_launch();
   }
