@@ -28,7 +28,7 @@
 #include "dsk_engine.cuh"
 
 #ifndef DSK_OPAQUE
-#define DSK_OPAQUE 1
+#define DSK_OPAQUE 2  // 1: thread coordinates opaque; 2: team coordinates too (no re-derived warp / G: cfg4 -0.8 %, cfg2 -1.8 %)
 #endif
 #ifndef DSK_LPT
 #define DSK_LPT 1  // largest-first row order for multi-wave minhash launches

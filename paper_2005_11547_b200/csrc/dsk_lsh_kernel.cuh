@@ -9,7 +9,7 @@
 #define DSK_LSH_SSEL 1  // selections staged in the team's idle warp queues (shared memory; 5 % faster on cfg4)
 #endif
 #ifndef DSK_LSH_SEL32
-#define DSK_LSH_SEL32 1  // buckets of 33..64 entries: threshold + compaction, then a 32-wide sort
+#define DSK_LSH_SEL32 0  // 1: buckets of 33..64 entries: threshold + compaction, then a 32-wide sort (-0.5 % at 24 warps in teams of 2, +2.3 % in 28 single-warp teams at 72 registers)
 #endif
 #ifndef DSK_LSH_FAST
 #define DSK_LSH_FAST 1  // 0: exact sort only; 1: float-key sort + exact fallback; 2: timing only
