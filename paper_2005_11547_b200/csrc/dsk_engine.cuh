@@ -50,10 +50,13 @@ namespace dsk {
 #define DSK_WARPS 24
 #endif
 #ifndef DSK_RUN
-#define DSK_RUN 3
+#define DSK_RUN 3  // areas per walker run (the minhash sink: DSK_RUN_MH)
+#endif
+#ifndef DSK_RUN_MH
+#define DSK_RUN_MH 2  // cfg3 k = 64: 22.9 -> 22.4 ms, cfg5 -0.6 %; the LSH sink prefers 3
 #endif
 #ifndef DSK_DIRECT
-#define DSK_DIRECT 1  // 0: off, 1: only when the rank depth is 0, 2: always when tables fit
+#define DSK_DIRECT 2  // 0: off, 1: only when the rank depth is 0, 2: always when tables fit (cfg2 on 24 x 3: 23.4 -> 22.4 ms)
 #endif
 #ifndef DSK_REFILL
 #define DSK_REFILL 8
@@ -86,7 +89,7 @@ constexpr int kQR = 64 * kILP;  // region / area ring capacity (>= 31 + kStep); 
 constexpr int kQ = 64 * kILP;   // hit ring capacity (>= kStep - 1 + kStep); power of two
 constexpr int kJs = 64;      // folded (j, stream) table rows; Poisson counts < 64
 constexpr int kRwin = 64;    // per-pass rank-window table entries (nu, rho)
-constexpr int kRun = DSK_RUN;  // areas per walker run on the direct (rho = 0) path
+// (areas per walker run on the direct (rho = 0) path: Sink::kRun)
 constexpr int kSeekTab = 256;  // walker seek table entries (per team, after the rank-window table)
 constexpr int kRwinStride = kRwin + kSeekTab / 16;  // uint4 units per rank-window block incl. the seek table
 
@@ -235,6 +238,7 @@ __device__ __forceinline__ uint32_t add_sat(uint32_t a, uint32_t b) {
 // nothing (the caller redoes the set with the general engine).
 template <class Sink, bool kFull, bool kDirect = false>
 struct Engine {
+  static constexpr int kRun = Sink::kRun;
   const SmemTables &T;
   WarpQueues &Q;
   // per-pass rank windows by (nu, rho): {r_hi + 1, r_lo | hasprev << 31,

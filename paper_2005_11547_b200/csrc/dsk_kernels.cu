@@ -234,6 +234,7 @@ __device__ __forceinline__ void team_sync(int G, int team) {
 template <bool kGlobal>  // slots in global memory (k too large for shared memory)
 struct MinhashSink {
   static constexpr bool kFuse = true;
+  static constexpr int kRun = DSK_RUN_MH;
   uint64_t *slots;  // 2*k words: {rank bits, fingerprint} per slot, 16-B aligned
   ModU32 md;
   unsigned int *filled;
@@ -601,6 +602,7 @@ constexpr int64_t kSliceElems = 4096;  // element index field of the row sink (1
 
 struct RowSink {
   static constexpr bool kFuse = true;
+  static constexpr int kRun = DSK_RUN;
   const DartsArgs *a;
   int64_t set, lo;
   unsigned long long *cursor;  // shared per warp
