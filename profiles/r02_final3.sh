@@ -14,7 +14,5 @@ bash profiles/quick_all.sh 2>&1 | head -7 > gpurun_out/quick_all.txt; cat gpurun
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg4.csv python bench.py --steps 2 --warmup 1 --no-cpu --no-e2e > gpurun_out/ncu_launch.log 2>&1; echo ncu-launch rc=$?
 SKIP=6 bash profiles/ncu_capture.sh r02f_lsh_cfg4 lsh_kernel --workload cfg4 --sets 200000
 SKIP=3 bash profiles/ncu_capture.sh r02f_mh_cfg2 minhash_kernel --workload cfg2
-SKIP=6 bash profiles/ncu_capture.sh r02f_mh_cfg3_k1024 minhash_kernel --workload cfg3 --k 1024 --sets 200000
-SKIP=3 bash profiles/ncu_capture.sh r02f_mh_cfg5 minhash_kernel --workload cfg5 --sets 1000000
 timeout 1200 python profiles/acceptance_shapes.py > gpurun_out/acceptance_shapes.json 2> gpurun_out/acceptance.err; echo acc rc=$?
 timeout 2400 python tests/parity_report.py --out gpurun_out/parity_report.json > gpurun_out/parity_report.log 2>&1; echo parity rc=$?; tail -9 gpurun_out/parity_report.log
