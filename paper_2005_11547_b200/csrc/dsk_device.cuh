@@ -19,13 +19,34 @@ constexpr double kMaxAreas = 134217728.0;  // 2^27, ref/darthash.py:32
 constexpr double kCandClip = 1099511627776.0;  // 2^40, ref/darthash.py:36
 constexpr uint64_t kEmptyRank = ~0ULL;
 
+#ifndef DSK_FZ_HI
+#define DSK_FZ_HI 0  // 1: the high word's shifts as mul.hi (FMA pipe) instead of SHF (ALU pipe)
+#endif
+#if DSK_FZ_HI && defined(__CUDA_ARCH__)
+__device__ __forceinline__ uint64_t xorshr(uint64_t h, int s) {
+  const uint32_t lo = (uint32_t)h, hi = (uint32_t)(h >> 32);
+  uint32_t hs;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(hs) : "r"(hi), "r"(1u << (32 - s)));
+  const uint32_t l2 = __funnelshift_r(lo, hi, s) ^ lo, h2 = hs ^ hi;
+  return ((uint64_t)h2 << 32) | l2;
+}
+#endif
+
 // splitmix64 finalizer, ref/randomness.py:58-63
 __host__ __device__ __forceinline__ uint64_t finalize(uint64_t h) {
+#if DSK_FZ_HI && defined(__CUDA_ARCH__)
+  h = xorshr(h, 30);
+  h *= kMul1;
+  h = xorshr(h, 27);
+  h *= kMul2;
+  return xorshr(h, 31);
+#else
   h ^= h >> 30;
   h *= kMul1;
   h ^= h >> 27;
   h *= kMul2;
   return h ^ (h >> 31);
+#endif
 }
 
 // 2^e for e in [-1022, 1023], exact
