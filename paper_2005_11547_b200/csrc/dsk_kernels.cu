@@ -1445,9 +1445,13 @@ static void plan_chunks(const int64_t *indptr, int64_t n, size_t cap, int64_t *b
   *nchunks = m - 1;
 }
 
-static size_t host_chunk_cap() {
-  size_t mb = 64;  // measured on cfg2: 64 MB 32.1 ms/step e2e, 128 MB 32.8, 256 MB 34.8
-  if (const char *e = getenv("DSK_CHUNK_MB")) mb = atoi(e) > 0 ? (size_t)atoi(e) : 64;
+// Largest chunk in MB of input.  Minhash, measured on cfg2: 64 MB 32.1 ms/step
+// e2e, 128 MB 32.8, 256 MB 34.8.  LSH (two launches and a compaction per
+// chunk, ~85 ns of kernel time per input KB), measured on cfg4: 32 MB 186.9,
+// 64 MB 183.1, 128 MB 181.3, 192 MB 180.1, 256 MB 179.5.
+static size_t host_chunk_cap(size_t default_mb) {
+  size_t mb = default_mb;
+  if (const char *e = getenv("DSK_CHUNK_MB")) mb = atoi(e) > 0 ? (size_t)atoi(e) : default_mb;
   return mb << 20;
 }
 
@@ -1578,10 +1582,11 @@ struct OutCopies {
 template <class Launch, class Out>
 static int host_pipeline(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
                          const double *weights, int64_t n, int64_t *dp, uint64_t *di, double *dw,
-                         int compute_streams, size_t out_row_bytes, Launch launch, Out out) {
+                         int compute_streams, size_t out_row_bytes, Launch launch, Out out,
+                         size_t chunk_mb = 64) {
   int64_t bounds[kMaxChunks + 1];
   int nch = 0;
-  plan_chunks(indptr, n, host_chunk_cap(), bounds, kMaxChunks + 1, &nch);
+  plan_chunks(indptr, n, host_chunk_cap(chunk_mb), bounds, kMaxChunks + 1, &nch);
   cudaStream_t cp = c->hs[0], os = c->hs[2];
   OutCopies d2h;
   d2h.c = c;

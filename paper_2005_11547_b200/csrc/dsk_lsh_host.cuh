@@ -192,5 +192,5 @@ extern "C" int dsk_lsh_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_
   };
   const size_t row_bytes = (out_keys ? (size_t)L * 8 : 0) + (out_fps ? (size_t)L * K * 8 : 0) +
                            4 + (phi ? 4 : 0) + (stats ? 16 : 0);
-  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, 2, row_bytes, launch, out);
+  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, 2, row_bytes, launch, out, 256);
 }
