@@ -1445,8 +1445,14 @@ static void plan_chunks(const int64_t *indptr, int64_t n, size_t cap, int64_t *b
   *nchunks = m - 1;
 }
 
-// Largest chunk in MB of input.  Minhash, measured on cfg2: 64 MB 32.1 ms/step
-// e2e, 128 MB 32.8, 256 MB 34.8.  LSH (two launches and a compaction per
+// Largest chunk in MB of input.  Minhash, measured on cfg2 (pinned / plain
+// numpy): 16 MB 31.6 / 35.6 ms/step e2e, 24 MB 31.6 / 34.1, 32 MB 31.4 / 35-37,
+// 48 MB 32.4 / 42.4, 64 MB 32.2 / 40.8, 128 MB 32.3 / 42.3; cfg3 k = 64: 32 MB
+// 26.6 / 35.5, 64 MB 27.2 / 44.2.  Batches of skewed row sizes (cfg5) take
+// 512 MB chunks: a launch lasts at least as long as its largest set takes on
+// one single-warp team (~17 ms for 16384 elements), so short launches are all
+// tail -- 2e6 cfg5 sets: 64 MB 499 ms, 256 MB 296, 512 MB 236, 1 GB 232
+// (device-resident 152).  LSH (two launches and a compaction per
 // chunk, ~85 ns of kernel time per input KB), measured on cfg4: 32 MB 186.9,
 // 64 MB 183.1, 128 MB 181.3, 192 MB 180.1, 256 MB 179.5.
 static size_t host_chunk_cap(size_t default_mb) {
@@ -1743,7 +1749,8 @@ extern "C" int dsk_minhash_csr_host(dsk_ctx *c, const int64_t *indptr, const uin
   if (const char *e = getenv("DSK_HOST_STREAMS")) streams = atoi(e) == 1 ? 1 : 2;
   const size_t row_bytes = (out_values ? (size_t)k * 8 : 0) + (out_bits ? (size_t)words * 8 : 0) +
                            4 + (phi ? 4 : 0) + (stats ? 16 : 0);
-  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, streams, row_bytes, launch, out);
+  return host_pipeline(c, indptr, ids, weights, n, dp, di, dw, streams, row_bytes, launch, out,
+                       skewed ? 512 : 32);
 }
 
 #include "dsk_lsh_host.cuh"
