@@ -36,6 +36,9 @@
 #ifndef DSK_LSH_DIRECT_KERNEL
 #define DSK_LSH_DIRECT_KERNEL 1  // LSH first launch on the direct-only engine specialisation
 #endif
+#ifndef DSK_MH_SPLIT_DEFAULT
+#define DSK_MH_SPLIT_DEFAULT 1  // size split of single-warp-team minhash launches (DSK_MH_SPLIT)
+#endif
 #ifndef DSK_OPAQUE_TB
 #define DSK_OPAQUE_TB 1  // LSH team block offsets opaque to the compiler (no rematerialisation)
 #endif
@@ -306,6 +309,10 @@ struct MinhashArgs {
   unsigned *retry_out_n;
   const uint32_t *retry_rows;
   const unsigned *retry_n;
+  // size split: this launch takes positions [*q_begin, *q_end) of the order
+  // (device values written by order_scatter_kernel; null: 0 / n)
+  const unsigned *q_begin;
+  const unsigned *q_end;
   TableArgs tabs;
 };
 
@@ -461,10 +468,13 @@ __global__ void __launch_bounds__(NW * 32, 1) minhash_kernel(MinhashArgs a) {
   for (;;) {
     if (tt == 0) {
       long long q = (long long)atomicAdd(a.counter, 1ULL);
-      if (a.retry_rows)  // second launch: the rows the direct-only launch handed back
+      if (a.retry_rows) {  // second launch: the rows the direct-only launch handed back
         C.set = q < (long long)*a.retry_n ? (long long)a.retry_rows[q] : a.n;
-      else
+      } else {
+        if (a.q_begin) q += (long long)*a.q_begin;
+        if (a.q_end && q >= (long long)*a.q_end) q = a.n;
         C.set = (a.order && q < a.n && *a.order_on) ? (long long)a.order[q] : q;
+      }
     }
     team_sync(G, team);
     const long long s = C.set;
@@ -1094,6 +1104,8 @@ static int scratch_release(dsk_ctx *c, int slot, cudaStream_t st) {
 // the heavy tail of Zipf-sized batches no longer finishes last).
 constexpr int kSizeClasses = 32;
 
+constexpr int kBigClass = 10;  // sets of >= 1024 elements go to the wide-team launch of a size split
+
 __device__ __forceinline__ int size_class(int64_t nnz) {
   return nnz <= 1 ? 0 : 63 - __clzll((unsigned long long)nnz);  // < 32 for nnz < 2^32
 }
@@ -1112,7 +1124,7 @@ __global__ void order_hist_kernel(const int64_t *indptr, int64_t n, unsigned *hi
 // cursor[kSizeClasses] receives the "skewed" flag: with all rows in one
 // size class the order stays the identity (the minhash kernel ignores it)
 __global__ void order_scatter_kernel(const int64_t *indptr, int64_t n, const unsigned *hist,
-                                     unsigned *cursor, uint32_t *order) {
+                                     unsigned *cursor, uint32_t *order, int big_class) {
   __shared__ unsigned start[kSizeClasses];
   __shared__ bool one_class;
   if (threadIdx.x == 0) {  // exclusive scan, largest class first
@@ -1123,7 +1135,12 @@ __global__ void order_scatter_kernel(const int64_t *indptr, int64_t n, const uns
       mx = hist[c] > mx ? hist[c] : mx;
     }
     one_class = (int64_t)mx == n;
-    if (blockIdx.x == 0) cursor[kSizeClasses] = one_class ? 0u : 1u;
+    if (blockIdx.x == 0) {
+      cursor[kSizeClasses] = one_class ? 0u : 1u;
+      // size split: rows of >= 2^kBigClass elements sit at order[0, nbig)
+      cursor[kSizeClasses + 1] = one_class ? 0u : start[big_class - 1];
+      cursor[kSizeClasses + 2] = (unsigned)n;
+    }
   }
   __syncthreads();
   if (one_class) return;
@@ -1194,6 +1211,8 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
   a.retry_out_n = nullptr;
   a.retry_rows = nullptr;
   a.retry_n = nullptr;
+  a.q_begin = nullptr;
+  a.q_end = nullptr;
   size_t smem = minhash_smem(k, G, NW, global_slots);
   int grid = c->num_sms;
   if ((int64_t)grid * (NW / G) > n) grid = (int)((n + (NW / G) - 1) / (NW / G));
@@ -1243,7 +1262,10 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
       CUDA_TRY(cudaMemsetAsync(hist, 0, 2 * kSizeClasses * 4 + 16, st));
       int og = (int)((n + 255) / 256 < 4 * c->num_sms ? (n + 255) / 256 : 4 * c->num_sms);
       order_hist_kernel<<<og, 256, 0, st>>>(indptr, n, hist); count_launch();
-      order_scatter_kernel<<<og, 256, 0, st>>>(indptr, n, hist, hist + kSizeClasses, order); count_launch();
+      int big_class = kBigClass;
+      if (const char *e = getenv("DSK_MH_SPLIT_CLASS"))
+        big_class = atoi(e) >= 1 && atoi(e) < kSizeClasses ? atoi(e) : kBigClass;
+      order_scatter_kernel<<<og, 256, 0, st>>>(indptr, n, hist, hist + kSizeClasses, order, big_class); count_launch();
       a.order = order;
       a.order_on = hist + 2 * kSizeClasses;
     }
@@ -1274,6 +1296,40 @@ extern "C" int dsk_minhash_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint6
     a.order_on = nullptr;
     a.retry_rows = retry_rows;
     a.retry_n = retry_cnt;
+  }
+  // Size split (single-warp-team shapes over rows of mixed sizes): a set of
+  // 16384 elements takes ~17 ms on one warp, which bounds the launch; the
+  // rows of >= 1024 elements (the head of the largest-first order) go to a
+  // first launch in teams of >= 4 warps, the rest to the single-warp launch.
+  {
+    const char *e = getenv("DSK_MH_SPLIT");
+    const bool want = e ? atoi(e) != 0 : DSK_MH_SPLIT_DEFAULT;
+    if (want && lpt && !direct_first && !global_slots && G == 1) {
+      int WNW = 0, WG = 0;
+      for (int nw : kWidths) {
+        for (int g = getenv("DSK_MH_SPLIT_G") ? atoi(getenv("DSK_MH_SPLIT_G")) : 4; g <= nw && !WNW; g++)
+          if (team_size_ok(g, nw) && minhash_smem(k, g, nw) <= c->max_smem) { WNW = nw; WG = g; }
+        if (WNW) break;
+      }
+      if (WNW) {
+        MinhashArgs b = a;
+        b.G = WG;
+        b.q_end = a.order_on + 1;  // nbig
+        unsigned long long *cw = c->d_counter + (c->next_slot.fetch_add(1) % kCounterSlots);
+        CUDA_TRY(cudaMemsetAsync(cw, 0, sizeof(unsigned long long), st));
+        b.counter = cw;
+        const size_t wsm = minhash_smem(k, WG, WNW);
+        switch (WNW) {
+          case 24: minhash_kernel<24><<<c->num_sms, 24 * 32, wsm, st>>>(b); break;
+          case 22: minhash_kernel<22><<<c->num_sms, 22 * 32, wsm, st>>>(b); break;
+          default: minhash_kernel<20><<<c->num_sms, 20 * 32, wsm, st>>>(b); break;
+        }
+        count_launch();
+        CUDA_TRY(cudaGetLastError());
+        a.q_begin = a.order_on + 1;
+        a.q_end = a.order_on + 2;
+      }
+    }
   }
   if (global_slots) {
     minhash_kernel<20, true><<<grid, 20 * 32, smem, st>>>(a); count_launch();

@@ -476,3 +476,36 @@ def test_minhash_direct_first_handoff(monkeypatch):
     tp, ti, tw = on_dev(p5, i5, w5)
     assert _batch_hint(tp, tp, ti, tw, tw, f, dev) & ~HINT_DIRECT == 0
     assert _batch_hint(p5, tp, ti, w5, tw, f, dev) == _batch_hint(tp, tp, ti, tw, tw, f, dev)
+
+
+@pytest.mark.gpu
+def test_minhash_size_split_equals_plain(monkeypatch):
+    """Size split of single-warp-team launches (DSK_MH_SPLIT): the rows of
+    >= 1024 elements (head of the largest-first order) go to a wide-team
+    launch, the rest to the single-warp launch; outputs equal the unsplit
+    launch's and the oracle's on the largest rows."""
+    import torch
+    from paper_2005_11547_b200 import HashFamily, _lib, as_u64, minhash_batch
+    n, k = 30000, 128
+    indptr, ids, w = workloads.generate("cfg5", n=n, start=4242)
+    assert int(np.diff(indptr).max()) >= 4096  # the batch holds large sets
+    f = HashFamily(4)
+    lib = _lib.load()
+    outs, launches = [], []
+    for env in ("0", "1"):
+        monkeypatch.setenv("DSK_MH_SPLIT", env)
+        l0 = lib.dsk_launch_count()
+        r = minhash_batch(indptr, ids, w, k, f, bits=True)
+        torch.cuda.synchronize()
+        launches.append(lib.dsk_launch_count() - l0)
+        outs.append(r)
+    assert launches[1] == launches[0] + 1  # the wide-team launch
+    for a, b in ((outs[0].values, outs[1].values), (outs[0].bits, outs[1].bits),
+                 (outs[0].phi, outs[1].phi), (outs[0].stats[:, 2:], outs[1].stats[:, 2:])):
+        assert torch.equal(a, b)
+    rows = np.argsort(np.diff(indptr))[-12:]
+    sp, si, sw = workloads.subset(indptr, ids, w, rows)
+    vals, status, phi, _ = Oracle(4).minhash_csr(sp, si, sw, k)
+    assert (status == 0).all()
+    assert np.array_equal(as_u64(outs[1].values)[rows], vals)
+    assert np.array_equal(outs[1].phi.cpu().numpy()[rows], phi)
