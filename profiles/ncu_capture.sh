@@ -8,6 +8,6 @@
 NAME=$1; KREG=$2; shift 2
 CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu $*"
 timeout 900 $CMD > gpurun_out/${NAME}_plain.json 2> gpurun_out/${NAME}_plain.err || { echo "plain run failed"; exit 1; }
-timeout 1800 ncu --set full --clock-control none --import-source on -k regex:$KREG -s ${SKIP:-3} -c 1 \
+timeout 1800 ncu --set full --clock-control none --import-source on -k regex:$KREG -s ${SKIP:-3} -c ${COUNT:-1} \
   -o gpurun_out/$NAME -f $CMD > gpurun_out/${NAME}_ncu.log 2>&1
 echo "ncu $NAME rc=$?"
