@@ -135,6 +135,17 @@ int dsk_lsh_csr(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
                 uint64_t *out_keys, uint64_t *out_fps, int32_t *status, int32_t *phi,
                 uint32_t *stats, void *stream);
 
+/* dsk_lsh_csr with a team-shape hint: max_row_hint = the largest row's
+ * element count (0 = unknown).  Results are identical.  Multi-wave batches
+ * run fastest in single-warp teams, but one very large set on one warp can
+ * bound the launch, so that shape is taken only for rows of <= 1024 elements
+ * (or, sizes unknown, for batches of >= 64 waves of teams).
+ * dsk_lsh_csr_host derives the hint from its host indptr. */
+int dsk_lsh_csr_ex(dsk_ctx *ctx, const int64_t *indptr, const uint64_t *ids,
+                   const double *weights, int64_t n, int32_t L, int32_t K, int32_t normalize,
+                   int64_t max_row_hint, uint64_t *out_keys, uint64_t *out_fps, int32_t *status,
+                   int32_t *phi, uint32_t *stats, void *stream);
+
 /* Host-buffer form of dsk_lsh_csr (same pipeline as dsk_minhash_csr_host).
  * LSH launches draw their per-team hit buffers from a pool of context-owned
  * slots reused in stream order, so concurrent calls on different streams

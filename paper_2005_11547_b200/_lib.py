@@ -92,6 +92,8 @@ SIGNATURES = [
     ("dsk_minhash_csr_host", ctypes.c_int, [_P, _P, _P, _P, _I64, _I32, _P, _P, _P, _P, _P]),
     ("dsk_lsh_csr", ctypes.c_int,
      [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P]),
+    ("dsk_lsh_csr_ex", ctypes.c_int,
+     [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _I64, _P, _P, _P, _P, _P, _P]),
     ("dsk_lsh_csr_host", ctypes.c_int,
      [_P, _P, _P, _P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P]),
     ("dsk_darts_csr", ctypes.c_int,

@@ -546,11 +546,18 @@ def lsh_batch(indptr, ids, weights, params: LshParams, hashes: HashFamily, *,
     status = torch.empty(n, dtype=torch.int32, device=dev)
     phi = torch.empty(n, dtype=torch.int32, device=dev)
     st = torch.empty((n, 4), dtype=torch.int32, device=dev) if stats else None
+    # team-shape hint (results never depend on it): the largest row, looked
+    # up (device arrays: one reduction + sync) only in the range of batch
+    # sizes where the shape depends on it
+    max_row = 0
+    if 16384 <= n < 400000:
+        max_row = int(np.diff(indptr).max()) if isinstance(indptr, np.ndarray) else \
+            int((p[1:] - p[:-1]).max())
     with torch.cuda.device(dev):
-        _lib.check(_lib.load().dsk_lsh_csr(
+        _lib.check(_lib.load().dsk_lsh_csr_ex(
             hashes.context(dev), _ptr(p), _ptr(i), _ptr(w), n, L, K, int(bool(normalize)),
-            _ptr(out_k), _ptr(out_f), _ptr(status), _ptr(phi), _ptr(st), _stream_ptr(dev)),
-            "dsk_lsh_csr")
+            max_row, _ptr(out_k), _ptr(out_f), _ptr(status), _ptr(phi), _ptr(st),
+            _stream_ptr(dev)), "dsk_lsh_csr")
     res = LshBatch(out_k, out_f, status, phi, st)
     if check:
         raise_for_status(status, dup_rows=_dup_rows(p, i))

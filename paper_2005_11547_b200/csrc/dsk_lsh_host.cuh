@@ -4,6 +4,15 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
                            const double *weights, int64_t n, int32_t L, int32_t K,
                            int32_t normalize, uint64_t *out_keys, uint64_t *out_fps,
                            int32_t *status, int32_t *phi, uint32_t *stats, void *stream) {
+  return dsk_lsh_csr_ex(c, indptr, ids, weights, n, L, K, normalize, 0, out_keys, out_fps, status,
+                        phi, stats, stream);
+}
+
+extern "C" int dsk_lsh_csr_ex(dsk_ctx *c, const int64_t *indptr, const uint64_t *ids,
+                              const double *weights, int64_t n, int32_t L, int32_t K,
+                              int32_t normalize, int64_t max_row_hint, uint64_t *out_keys,
+                              uint64_t *out_fps, int32_t *status, int32_t *phi, uint32_t *stats,
+                              void *stream) {
   if (!c || !indptr || !status || n < 0) return set_err(DSK_EARG, "bad argument");
   if (L < 1 || K < 1) return set_err(DSK_EARG, "L and K must be positive");  // ref/annindex.py:33-34
   if (n == 0) return DSK_OK;
@@ -43,7 +52,14 @@ extern "C" int dsk_lsh_csr(dsk_ctx *c, const int64_t *indptr, const uint64_t *id
     // no chunk hand-out; cfg4: 28 x 1 is 3.6 % faster than 14 x 2), else the
     // general shape's team size.  DSK_LSH_DG: tuning
     const char *eg = getenv("DSK_LSH_DG");
-    int cand[2] = {n >= 4 * (int64_t)c->num_sms * 28 ? 1 : G, G};
+    // ... unless a large set would bound the launch: a set takes ~1-2 us per
+    // element on one warp (30 k cfg5 rows, largest 16384: 22.9 ms in
+    // single-warp teams against 15.1 in teams of 2; 300 k rows: 82.7 against
+    // 84.5), so single-warp teams need rows of <= 1024 elements
+    // (max_row_hint) or, sizes unknown, a batch of >= 64 waves
+    const int64_t wave = (int64_t)c->num_sms * 28;
+    const bool single = n >= 4 * wave && (max_row_hint > 0 ? max_row_hint <= 1024 : n >= 64 * wave);
+    int cand[2] = {single ? 1 : G, G};
     if (eg && atoi(eg) >= 1) cand[0] = cand[1] = atoi(eg);
     DNW = 0;
     for (int q = 0; q < 2 && !DNW; q++)
@@ -176,10 +192,12 @@ extern "C" int dsk_lsh_csr_host(dsk_ctx *c, const int64_t *indptr, const uint64_
   int32_t *ds = (int32_t *)(base + off_s);
   int32_t *dph = phi ? (int32_t *)(base + off_ph) : nullptr;
   uint32_t *dst = stats ? (uint32_t *)(base + off_st) : nullptr;
+  int64_t max_row = 1;  // team-shape hint of dsk_lsh_csr_ex
+  for (int64_t r = 0; r < n; r++) max_row = indptr[r + 1] - indptr[r] > max_row ? indptr[r + 1] - indptr[r] : max_row;
   auto launch = [&](int64_t r0, int64_t m, cudaStream_t st) {
-    return dsk_lsh_csr(c, dp + r0, di, dw, m, L, K, normalize, dk ? dk + r0 * L : nullptr,
-                       df ? df + r0 * L * K : nullptr, ds + r0, dph ? dph + r0 : nullptr,
-                       dst ? dst + r0 * 4 : nullptr, st);
+    return dsk_lsh_csr_ex(c, dp + r0, di, dw, m, L, K, normalize, max_row,
+                          dk ? dk + r0 * L : nullptr, df ? df + r0 * L * K : nullptr, ds + r0,
+                          dph ? dph + r0 : nullptr, dst ? dst + r0 * 4 : nullptr, st);
   };
   auto out = [&](int64_t r0, int64_t m, cudaStream_t st, OutCopies &d2h) -> int {
     int rc2 = DSK_OK;
