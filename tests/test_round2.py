@@ -492,6 +492,7 @@ def test_minhash_size_split_equals_plain(monkeypatch):
     f = HashFamily(4)
     lib = _lib.load()
     outs, launches = [], []
+    monkeypatch.setenv("DSK_MH_DIRECT", "0")  # (a direct-first launch takes no size split)
     for env in ("0", "1"):
         monkeypatch.setenv("DSK_MH_SPLIT", env)
         l0 = lib.dsk_launch_count()
