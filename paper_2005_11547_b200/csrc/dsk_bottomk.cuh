@@ -54,6 +54,7 @@ struct BottomKArgs {
 struct BottomKSink {
   static constexpr bool kFuse = true;
   static constexpr int kRun = DSK_RUN;
+  static constexpr int kRunDeep = DSK_RUN;
   BkEntry *buf;
   uint32_t cap;
   const uint64_t *ids;  // ids of the current slice

@@ -55,6 +55,9 @@ namespace dsk {
 #ifndef DSK_RUN_MH
 #define DSK_RUN_MH 2  // cfg3 k = 64: 22.9 -> 22.4 ms, cfg5 -0.6 %; the LSH sink prefers 3
 #endif
+#ifndef DSK_RUN_MH_DEEP
+#define DSK_RUN_MH_DEEP 1  // minhash passes of rank depth >= 1 (general engine)
+#endif
 #ifndef DSK_DIRECT
 #define DSK_DIRECT 2  // 0: off, 1: only when the rank depth is 0, 2: always when tables fit (cfg2 on 24 x 3: 23.4 -> 22.4 ms)
 #endif
@@ -239,6 +242,13 @@ __device__ __forceinline__ uint32_t add_sat(uint32_t a, uint32_t b) {
 template <class Sink, bool kFull, bool kDirect = false>
 struct Engine {
   static constexpr int kRun = Sink::kRun;
+  // Walker run length of this pass: passes of rank depth >= 1 (cfg2: elements
+  // with a handful of rho = 0 areas each) hand out single areas when the sink
+  // asks for it (Sink::kRunDeep; cfg2 22.4 -> 21.6 ms), rank depth 0 runs of kRun
+  __device__ __forceinline__ uint32_t run_len() const {
+    return (!kDirect && Sink::kRunDeep != kRun && P.RD > 0) ? (uint32_t)Sink::kRunDeep
+                                                            : (uint32_t)kRun;
+  }
   const SmemTables &T;
   WarpQueues &Q;
   // per-pass rank windows by (nu, rho): {r_hi + 1, r_lo | hasprev << 31,
@@ -589,7 +599,9 @@ struct Engine {
         cnt0 = rw.z;
         lane_full = add_sat(lane_full, rw.w);
       }
-      nruns = (cnt0 + kRun - 1) / kRun;
+      nruns = (!kDirect && Sink::kRunDeep != kRun && P.RD > 0)
+                  ? (cnt0 + Sink::kRunDeep - 1) / Sink::kRunDeep
+                  : (cnt0 + kRun - 1) / kRun;
       dmeta = (uint32_t)(dtop & 0xff) | ((uint32_t)nu_v << 8);
       c = valid ? (uint32_t)(depth + 1) * (uint32_t)P.RD : 0;  // rho >= 1 regions
     } else {
@@ -650,10 +662,11 @@ struct Engine {
       uint32_t first = __shfl_sync(DSK_FULL, run_excl, src);
       if (idle && q < run_total) {
         uint2 d = Q.elD[src];
-        uint32_t a0 = (q - first) * kRun;
+        const uint32_t rl = run_len();
+        uint32_t a0 = (q - first) * rl;
         wk_slot = src;
         wk_a = a0;
-        wk_end = a0 + kRun < d.x ? a0 + kRun : d.x;
+        wk_end = a0 + rl < d.x ? a0 + rl : d.x;
         walker_seek(a0, (int)(d.y & 0xff));
       }
       uint32_t took = (uint32_t)__popc(idle_mask);

@@ -238,6 +238,7 @@ template <bool kGlobal>  // slots in global memory (k too large for shared memor
 struct MinhashSink {
   static constexpr bool kFuse = true;
   static constexpr int kRun = DSK_RUN_MH;
+  static constexpr int kRunDeep = DSK_RUN_MH_DEEP;
   uint64_t *slots;  // 2*k words: {rank bits, fingerprint} per slot, 16-B aligned
   ModU32 md;
   unsigned int *filled;
@@ -613,6 +614,7 @@ constexpr int64_t kSliceElems = 4096;  // element index field of the row sink (1
 struct RowSink {
   static constexpr bool kFuse = true;
   static constexpr int kRun = DSK_RUN;
+  static constexpr int kRunDeep = DSK_RUN;
   const DartsArgs *a;
   int64_t set, lo;
   unsigned long long *cursor;  // shared per warp

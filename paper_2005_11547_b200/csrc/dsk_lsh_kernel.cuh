@@ -40,6 +40,7 @@
 struct LshSink {
   static constexpr bool kFuse = DSK_LSH_FUSE != 0;
   static constexpr int kRun = DSK_RUN;
+  static constexpr int kRunDeep = DSK_RUN;
   ulonglong2 *buf;      // global: {fp, rank bits}, bucket b's first S hits at b*S
   ulonglong2 *ovf;      // global: hits beyond a bucket's S slots
   uint32_t *ovf_b;      // global: their buckets
