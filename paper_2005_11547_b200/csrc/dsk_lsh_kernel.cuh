@@ -34,13 +34,16 @@
 //                key, in order;
 //   epilogue     one lane per table folds the K fingerprints with mix64.
 
+#ifndef DSK_RUN_LSH_DEEP
+#define DSK_RUN_LSH_DEEP DSK_RUN  // walker run length of LSH passes of rank depth >= 1 (general engine: normalised sets)
+#endif
 #ifndef DSK_LSH_FUSE
 #define DSK_LSH_FUSE 1  // dart-0 fusion for the LSH sink (1.8 % faster since the per-bucket slots)
 #endif
 struct LshSink {
   static constexpr bool kFuse = DSK_LSH_FUSE != 0;
   static constexpr int kRun = DSK_RUN;
-  static constexpr int kRunDeep = DSK_RUN;
+  static constexpr int kRunDeep = DSK_RUN_LSH_DEEP;
   ulonglong2 *buf;      // global: {fp, rank bits}, bucket b's first S hits at b*S
   ulonglong2 *ovf;      // global: hits beyond a bucket's S slots
   uint32_t *ovf_b;      // global: their buckets
